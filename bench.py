@@ -1,0 +1,351 @@
+"""Benchmark of the B200 decision plane (driver contract: one JSON line).
+
+Default workload (N=1): BASELINE configs[1] — Qwen2.5 vocab V=152,064,
+B=1,024 fp32 logits, repetition/presence/frequency penalties + top-k/top-p/
+min-p, synthetic logits from the SyntheticSource formula generated on device.
+A step = one pass of the hot path over the batch: dp_sample_full (fused
+penalties -> tau -> top-k -> top-p -> min-p -> draw) + the penalty-state
+update (the reference's timed unit, harness.py:274-279).  With N GPUs each rank
+owns a fixed 1,024-row slice (weak scaling) and the step ends with the
+token-id all-gather over NCCL.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+                    [--config c2|c1|c3|c4|c5] [--variant full|shvs]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+C2_PARAMS = dict(temperature=0.8, top_k=50, top_p=0.9, min_p=0.05, rep_penalty=1.1,
+                 presence_penalty=0.5, frequency_penalty=0.1)
+C1_PARAMS = dict(temperature=0.8, top_k=50, top_p=0.9, rep_penalty=1.1)
+CONFIGS = {
+    "c1": dict(V=32000, B=64, dtype="f32", params=C1_PARAMS, name="llama2-32k-b64"),
+    "c2": dict(V=152064, B=1024, dtype="f32", params=C2_PARAMS, name="qwen2.5-152k-b1024"),
+    "c4": dict(V=151936, B=8192, dtype="f32", params=C2_PARAMS, name="qwen3-151936-b8192"),
+}
+METRIC = "sampled tokens/s at V=152k, B=1024; achieved HBM GB/s vs B200 peak"
+PROMPT_LEN = 32
+RESET_EVERY = 128  # harness.py:266-269
+
+
+def env_rank():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.samples, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm (oracle port of the reference algorithm, on host cores)
+
+def _cpu_worker(args):
+    x, prompts, params, it0, seconds = args
+    from oracle import decplane_oracle as O
+
+    v = x.shape[1]
+    states = [O.State.new(p, v) for p in prompts]
+    pp = O.Params(**params)
+    t0 = time.perf_counter()
+    n = 0
+    it = it0
+    while True:
+        for b in range(x.shape[0]):
+            u = O.pregenerate_slice(pp.seed, it, [b])[0]
+            d = O.sample_full_row(x[b], states[b], pp, u)
+            states[b].update(d.token)
+            n += 1
+        it += 1
+        if time.perf_counter() - t0 >= seconds:
+            break
+    return n, time.perf_counter() - t0
+
+
+def cpu_baseline(x_rows: np.ndarray, prompts, params, seconds: float, cores: int | None = None):
+    """The reference decision law (oracle port) timed on this host's cores: one
+    process per core, rows split by partition_batch (transport.py:133-144)."""
+    import multiprocessing as mp
+
+    cores = cores or len(os.sched_getaffinity(0))
+    parts = np.array_split(np.arange(x_rows.shape[0]), cores)
+    jobs = [(x_rows[p], [prompts[i] for i in p], params, 0, seconds) for p in parts if len(p)]
+    ctx = mp.get_context("fork")
+    with ctx.Pool(len(jobs)) as pool:
+        res = pool.map(_cpu_worker, jobs)
+    rows = sum(r[0] for r in res)
+    wall = max(r[1] for r in res)
+    return rows / wall, len(jobs), rows
+
+
+def reference_arm(args, cfg):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    from oracle import decplane_oracle as O
+
+    v = cfg["V"]
+    nrows = 64
+    src = O.Synthetic(v)
+    x = src.wire(0, range(nrows))
+    prompts = [np.random.default_rng(b).integers(0, v, PROMPT_LEN) for b in range(nrows)]
+    steps = []
+    # bounded: the whole --steps K --warmup W run stays within ~ref_budget seconds
+    per_step = max(0.25, min(args.ref_seconds, args.ref_budget / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        cpu_baseline(x, prompts, cfg["params"], per_step)
+    total_rows, total_t = 0, 0.0
+    for _ in range(args.steps):
+        rate, cores, rows = cpu_baseline(x, prompts, cfg["params"], per_step)
+        steps.append(rate)
+        total_rows += rows
+        total_t += rows / rate
+    value = total_rows / total_t
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * cfg["B"] / value,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (SyntheticSource formula, seed 0)",
+            "config": {"workload": cfg["name"], "V": v, "B": cfg["B"], "params": cfg["params"]},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port",
+                             "sample": f"{nrows} rows of the workload, {per_step:.2f}s per step, "
+                                       "oracle port of _Sampler.sample+update_output_histogram"},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    import build
+
+    if rank == 0:
+        build.build()
+    if world > 1:
+        dist.barrier()
+    from paper_2512_00719_b200 import DecisionPlane, SamplingParams
+    from paper_2512_00719_b200.synthetic import SyntheticSource
+
+    v, b_local = cfg["V"], cfg["B"]
+    if args.config == "c4":  # strong scaling: the global batch is fixed
+        from paper_2512_00719_b200 import partition_batch
+
+        lo, hi = partition_batch(cfg["B"], world)[rank]
+        b_local = hi - lo
+        row0 = lo
+        scaling = "strong"
+    else:
+        row0 = rank * b_local
+        scaling = "weak"
+    seq_ids = np.arange(row0, row0 + b_local, dtype=np.uint64)
+    prompts = [np.random.default_rng(int(s)).integers(0, v, PROMPT_LEN) for s in seq_ids]
+    params = [SamplingParams(**cfg["params"], seed=0)] * b_local
+    plane = DecisionPlane(v, params, prompts=prompts, seq_ids=seq_ids, device=dev,
+                          max_generated=RESET_EVERY + 8, split=args.split)
+    src = SyntheticSource(v, device=dev)
+    tdt = torch.float32 if cfg["dtype"] == "f32" else torch.bfloat16
+    bufs = [src.generate(i, seq_ids, dtype=tdt) for i in range(2)]   # 2 x 623 MB > L2
+    gathered = torch.empty(b_local * world, dtype=torch.int32, device=dev)
+    st = torch.cuda.current_stream()
+
+    it = [0]
+
+    def step(ev_pair=None):
+        i = it[0]
+        if i % RESET_EVERY == 0 and i > 0:
+            plane.state.reset()
+        if ev_pair is not None:
+            ev_pair[0].record(st)
+        d = plane.sample(bufs[i & 1], i, update=False)
+        if ev_pair is not None:
+            ev_pair[1].record(st)
+        plane.state.update(d.token, d.flags)
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, d.token)
+        it[0] += 1
+        return d
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        start.record(st)
+        for k in range(args.steps):
+            step(evs[k])
+        end.record(st)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    ms = start.elapsed_time(end)
+    kern_ms = [a.elapsed_time(b) for a, b in evs]
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    total_tokens = b_local * world * args.steps if scaling == "weak" else cfg["B"] * args.steps
+    value = total_tokens / (ms / 1000.0)
+
+    # roofline of the dominant kernel (dp_sample_full): algorithmic bytes / launch
+    pen_len = plane.state.len.float().mean().item()
+    esz = 4 if cfg["dtype"] == "f32" else 2
+    bytes_per_row = v * esz + 8 * pen_len + 4 + 64 + 8 + 13
+    kern_avg_s = statistics.mean(kern_ms) / 1000.0
+    achieved = bytes_per_row * b_local / kern_avg_s / 1e9
+    peak, peak_kind = measured_peak()
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            traffic = json.load(fh).get(f"{args.config}_{args.variant}")
+    except Exception:
+        pass
+
+    # e2e through the public API with host buffers (pinned), copies timed
+    e2e = None
+    if rank == 0 or world > 1:
+        host = bufs[0].cpu().pin_memory()
+        dbuf = torch.empty_like(bufs[0])
+        tok_host = torch.empty(b_local, dtype=torch.int32).pin_memory()
+        n_e2e = max(2, min(args.steps, 6))
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for k in range(n_e2e):
+            dbuf.copy_(host, non_blocking=True)
+            d = plane.sample(dbuf, 10_000 + k)
+            tok_host.copy_(d.token, non_blocking=True)
+        e1.record(st)
+        torch.cuda.synchronize()
+        e2e_s = e0.elapsed_time(e1) / 1000.0
+        e2e = {"value": b_local * world * n_e2e / e2e_s if scaling == "weak" else cfg["B"] * n_e2e / e2e_s,
+               "unit": "tokens/s", "h2d_bytes_per_step": int(host.numel() * host.element_size()),
+               "d2h_bytes_per_step": int(tok_host.numel() * 4), "steps": n_e2e}
+
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            x_rows = bufs[0][:64].float().cpu().numpy()
+            rate, cores, rows = cpu_baseline(x_rows, prompts[:64], cfg["params"], args.cpu_seconds)
+            cpu = {"value": rate, "unit": "tokens/s", "cores": cores, "kind": "port",
+                   "sample": f"64 rows of this workload looped for {args.cpu_seconds:.0f}s on {cores} processes "
+                             f"({rows} decisions), oracle port of _Sampler.sample+update_output_histogram"}
+        line = {
+            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": scaling,
+            "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic (SyntheticSource formula on device)",
+            "config": {"workload": cfg["name"], "V": v, "B_per_gpu": b_local, "variant": args.variant,
+                       "params": cfg["params"], "l2": "inputs larger than L2 (2 x batch buffers alternate)",
+                       "split": plane._plan.split},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                         "kernel": "dp_sample_full (topk_sample_kernel)", "kernel_ms": statistics.mean(kern_ms),
+                         "bytes_per_row": bytes_per_row},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": args.steps * (3 + (1 if world > 1 else 0)) + sum(
+                1 for i in range(args.warmup, args.warmup + args.steps) if i % RESET_EVERY == 0 and i > 0),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--variant", default="full", choices=["full", "shvs"])
+    ap.add_argument("--split", type=int, default=0)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--ref-seconds", type=float, default=5.0)
+    ap.add_argument("--ref-budget", type=float, default=90.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        reference_arm(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

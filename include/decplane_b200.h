@@ -1,0 +1,187 @@
+/*
+ * decplane_b200.h — C ABI of the B200-native decision plane (sampling epilogue).
+ *
+ * Drop-in boundary for the reference's sampler surface (arXiv 2512.00719,
+ * reference package `decplane`, /root/reference/pkg/src/decplane).  The
+ * reference exposes this path only as Python calls; each entry point below
+ * names the reference interface it replaces.  All pointers are DEVICE pointers
+ * unless the parameter name ends in `_host`; every call is stream-ordered on
+ * `stream` (a cudaStream_t passed as void*), never synchronises, and returns
+ * DP_OK (0) or a negative dp_status_t.  Per-row problems are reported in the
+ * per-row `flags` byte instead of exceptions (the Python host layer turns
+ * them into DegenerateRowError / RangeError like core.py:15-20).
+ *
+ * Layout conventions
+ *   logits   row-major [B, ld] (ld >= V), fp32 or bf16.  This is byte-identical
+ *            to the reference's "vocabulary-major" shard of one TP rank
+ *            (core.py:184-199: (V, B) in Fortran order).
+ *   hot-first rows (SHVS): position p < H holds hot id perm[p] in hot order,
+ *            positions H..V-1 hold the tail ids in ascending order
+ *            (shvs.py:37-92).  perm maps position -> token id, inv_perm the
+ *            inverse.  Identity layout = perm NULL.
+ */
+#ifndef DECPLANE_B200_H
+#define DECPLANE_B200_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define DP_API __attribute__((visibility("default")))
+#else
+#define DP_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  DP_OK = 0,
+  DP_ERR_ARG = -1,          /* invalid argument (ValueError in the reference)   */
+  DP_ERR_CUDA = -2,         /* CUDA launch / runtime failure                    */
+  DP_ERR_UNSUPPORTED = -3,  /* shape or dtype outside what this build supports  */
+  DP_ERR_CAPACITY = -4      /* a fixed-capacity buffer would overflow           */
+} dp_status_t;
+
+typedef enum { DP_F32 = 0, DP_BF16 = 1 } dp_dtype_t;
+
+/* per-row flag bits */
+#define DP_FLAG_ACCEPTED_HOT   0x02u  /* SHVS took the hot path (TokenDecision.accepted_hot) */
+#define DP_FLAG_NEAR_BOUNDARY  0x04u  /* a draw / accept / top-p / min-p decision was within
+                                         1e-6 of its flip point (logged by the host)          */
+#define DP_FLAG_REJECTED       0x08u  /* SHVS rejected the hot proposal -> tail pass           */
+#define DP_FLAG_PEN_OVERFLOW   0x40u  /* penalty list full; token not recorded                */
+#define DP_FLAG_DEGENERATE     0x80u  /* no usable probability mass (DegenerateRowError)      */
+
+/* SamplingParams (core.py:23-34), one per row. top_k 0 = disabled. 64 bytes. */
+typedef struct {
+  double   temperature;
+  int32_t  top_k;
+  int32_t  reserved;
+  double   top_p;
+  double   min_p;
+  double   rep_penalty;
+  double   presence_penalty;
+  double   frequency_penalty;
+  uint64_t seed;
+} dp_params_t;
+
+/* Sparse, device-resident SequenceState (core.py:100-169).  Row b owns
+ * entries [b*cap, b*cap+len[b]) of ids/out_count: every token in prompt ∪
+ * output (the reference's touched_ids) with its output count (0 = prompt
+ * only).  prompt_len[b] entries form the prompt prefix (for reset). */
+typedef struct {
+  int32_t* ids;
+  int32_t* out_count;
+  int32_t* len;
+  int32_t* prompt_len;
+  int32_t  cap;
+  int32_t  vocab_size;
+} dp_penalty_t;
+
+/* Optional per-row diagnostics (any field may be NULL). */
+typedef struct {
+  int32_t* topk_ids;     /* [B, topk_stride] top-k stage ids, sorted (value desc, id asc) */
+  double*  topk_ready;   /* [B, topk_stride] their sampling-ready values (penalized / tau) */
+  int32_t  topk_stride;
+  int32_t  reserved;
+  double*  margin;       /* [B] distance of the closest decision to its flip point        */
+  int32_t* kept;         /* [B] candidates surviving top-k/top-p/min-p                     */
+  double*  alpha;        /* [B] SHVS hot mass alpha (shvs.py:148-154)                      */
+  uint64_t* bytes_touched; /* [B] logits bytes streamed for the row (VisitCounter analogue) */
+} dp_debug_t;
+
+/* Launch plan supplied by the host (nullable -> conservative defaults).
+ * max_top_k: upper bound of top_k over the rows of the call (0 = unknown);
+ * rows whose top-k stage does not fit the planned capacity take the general
+ * (radix) path, so the bound only affects speed, never results.
+ * split: CTAs per row cluster for the streaming kernels (0 = auto, <= 8). */
+typedef struct {
+  int32_t max_top_k;
+  int32_t split;
+  int32_t reserved[6];
+} dp_plan_t;
+
+/* Library / device info. dp_device_check returns DP_OK when `device` is sm_100. */
+DP_API int dp_version(void);
+DP_API int dp_device_check(int device);
+/* Human-readable reason of the last failing call on this thread. */
+DP_API const char* dp_last_error(void);
+
+/* rng.pregenerate_slice (rng.py:94-113), keyed per row by params[b].seed:
+ * out[b,0..2] = (u_hot, u_accept, u_tail) for (seed_b, iteration, seq_ids[b]). */
+DP_API int dp_uniforms(const dp_params_t* params, const uint64_t* seq_ids, int64_t B,
+                uint64_t iteration, double* out, void* stream);
+
+/* Full-vocabulary decision: _Sampler("offload-truncate").sample for every row
+ * (service.py:381-409) == sample_full (filtering.py:172-201) token law:
+ * penalties (penalty.py:66-78) -> /tau (service.py:236-241) -> top-k -> top-p
+ * -> min-p (filtering.py:61-105) -> inverse-CDF draw with u_hot
+ * (filtering.py:158-162).  uniforms may be NULL: then they are derived on
+ * device from (params[b].seed, iteration, seq_ids[b]) exactly as dp_uniforms. */
+DP_API int dp_sample_full(const void* logits, int dtype, int64_t B, int64_t V, int64_t ld,
+                   const dp_params_t* params, const dp_penalty_t* pen_host,
+                   const double* uniforms, const uint64_t* seq_ids, uint64_t iteration,
+                   int32_t* token, double* logprob, uint8_t* flags,
+                   const dp_debug_t* debug_host, const dp_plan_t* plan_host, void* stream);
+
+/* Producer summary: make_shard_blocks' per-row (row_max, total_expsum) over the
+ * penalized, temperature-scaled row (service.py:470-504, shvs.py:157-168).
+ * Layout-agnostic (a permutation does not change max or sum). */
+DP_API int dp_row_summary(const void* logits, int dtype, int64_t B, int64_t V, int64_t ld,
+                   const dp_params_t* params, const dp_penalty_t* pen_host,
+                   const int32_t* inv_perm, double* row_max, double* total_expsum,
+                   void* stream);
+
+/* Speculative hot-vocab sampling on hot-first rows: split_decision
+ * (shvs.py:198-255) as driven by _Sampler SHVS (service.py:354-380).  Touches
+ * H positions per row, plus V-H on rejection.  scratch_rows: device int32
+ * [B + 1] workspace for the on-device reject list. */
+DP_API int dp_sample_shvs(const void* logits_hotfirst, int dtype, int64_t B, int64_t V, int64_t H,
+                   int64_t ld, const int32_t* perm, const int32_t* inv_perm,
+                   const double* row_max, const double* total_expsum,
+                   const dp_params_t* params, const dp_penalty_t* pen_host,
+                   const double* uniforms, const uint64_t* seq_ids, uint64_t iteration,
+                   int32_t* token, double* logprob, uint8_t* flags,
+                   const dp_debug_t* debug_host, const dp_plan_t* plan_host,
+                   int32_t* scratch_rows, void* stream);
+
+/* update_output_histogram (penalty.py:18-32) for every row: C_o[tok] += 1,
+ * first-seen ids appended.  Rows whose flags[b] has DP_FLAG_DEGENERATE are
+ * skipped; a full list sets DP_FLAG_PEN_OVERFLOW. flags may be NULL. */
+DP_API int dp_penalty_update(const dp_penalty_t* pen_host, const int32_t* token, int64_t B,
+                      uint8_t* flags, void* stream);
+
+/* Reset rows to their prompt-only state (new_sequence_state, core.py:144-169). */
+DP_API int dp_penalty_reset(const dp_penalty_t* pen_host, int64_t B, void* stream);
+
+/* apply_penalties(...)/tau materialised as f64 rows (ReadyColumn.full,
+ * service.py:236-241).  Debug / parity use. */
+DP_API int dp_ready_rows(const void* logits, int dtype, int64_t B, int64_t V, int64_t ld,
+                  const dp_params_t* params, const dp_penalty_t* pen_host,
+                  double* out, void* stream);
+
+/* SyntheticSource (service.py:429-467): base_by_id[V] (f64) + noise * Gumbel
+ * keyed by (seed, DOMAIN_LOGITS, iteration, seq_ids[b], v), written as
+ * fp32 or bf16 rows; perm (position -> id, may be NULL) writes hot-first rows. */
+DP_API int dp_synth_logits(const double* base_by_id, double noise, uint64_t seed, uint64_t iteration,
+                    const uint64_t* seq_ids, int64_t B, int64_t V, int64_t ld, const int32_t* perm,
+                    int dtype, void* out, void* stream);
+
+/* Batch hit-ratio curve (sizing.estimate_hit_ratio_curve, sizing.py:78-100):
+ * out[b, g] = mass of the first grid[g] hot positions of the ready row. */
+DP_API int dp_hot_mass_curve(const void* logits_hotfirst, int dtype, int64_t B, int64_t V, int64_t ld,
+                      const double* row_max, const double* total_expsum,
+                      const dp_params_t* params, const dp_penalty_t* pen_host,
+                      const int32_t* inv_perm, const int32_t* grid, int32_t n_grid,
+                      double* out, void* stream);
+
+/* Token-id all-gather across batch shards (DecisionLedger, transport.py:400-433):
+ * ncclAllGather of int32 tokens over the communicator `nccl_comm` (an
+ * ncclComm_t).  Implemented in the host layer via torch.distributed; kept in
+ * the ABI for non-Python callers that link NCCL themselves. */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DECPLANE_B200_H */

@@ -1,0 +1,149 @@
+// aux_kernels.cu — per-row uniforms, penalty-state maintenance, debug ready
+// rows and the synthetic logits producer.
+#include "common.cuh"
+
+namespace dp {
+
+// rng.pregenerate_slice per row (rng.py:94-113; seed per row: service.py:761)
+__global__ void uniforms_kernel(const dp_params_t* params, const uint64_t* seq_ids, int64_t B,
+                                uint64_t iteration, double* out) {
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  double u[3];
+  row_uniforms(params[b].seed, iteration, seq_ids[b], u);
+  out[3 * b] = u[0];
+  out[3 * b + 1] = u[1];
+  out[3 * b + 2] = u[2];
+}
+
+// update_output_histogram (penalty.py:18-32): one warp per row scans the
+// row's sparse list; hit -> count+1, miss -> append (id, 1).
+__global__ void penalty_update_kernel(dp_penalty_t pen, const int32_t* token, int64_t B,
+                                      uint8_t* flags) {
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (row >= B) return;
+  const uint32_t lane = threadIdx.x & 31u;
+  if (flags && (flags[row] & DP_FLAG_DEGENERATE)) return;
+  const int32_t tok = token[row];
+  if (tok < 0 || tok >= pen.vocab_size) {
+    if (lane == 0 && flags) flags[row] |= DP_FLAG_DEGENERATE;
+    return;
+  }
+  int32_t* ids = pen.ids + row * pen.cap;
+  int32_t* cnt = pen.out_count + row * pen.cap;
+  const int32_t len = pen.len[row];
+  int32_t hit = -1;
+  for (int32_t base = 0; base < len && hit < 0; base += 32) {
+    const int32_t j = base + lane;
+    const uint32_t m = __ballot_sync(0xffffffffu, j < len && ids[j] == tok);
+    if (m) hit = base + __ffs(m) - 1;
+  }
+  if (lane == 0) {
+    if (hit >= 0) {
+      cnt[hit] += 1;
+    } else if (len < pen.cap) {
+      ids[len] = tok;
+      cnt[len] = 1;
+      pen.len[row] = len + 1;
+    } else if (flags) {
+      flags[row] |= DP_FLAG_PEN_OVERFLOW;
+    }
+  }
+}
+
+// new_sequence_state (core.py:144-169): keep the prompt prefix, zero counts
+__global__ void penalty_reset_kernel(dp_penalty_t pen, int64_t B) {
+  const int64_t row = blockIdx.x;
+  if (row >= B) return;
+  const int32_t pl = pen.prompt_len[row];
+  for (int32_t j = threadIdx.x; j < pl; j += blockDim.x) pen.out_count[row * pen.cap + j] = 0;
+  if (threadIdx.x == 0) pen.len[row] = pl;
+}
+
+// ReadyColumn.full (service.py:236-241) materialised in f64
+template <typename T>
+__global__ void ready_rows_kernel(const T* logits, int64_t V, int64_t ld, const dp_params_t* params,
+                                  dp_penalty_t pen, double* out) {
+  const int64_t row = blockIdx.y;
+  const dp_params_t p = params[row];
+  const T* x = logits + row * ld;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x)
+    out[row * V + v] = ready_plain(Elem<T>::get(x, v), p);
+}
+template <typename T>
+__global__ void ready_rows_pen_kernel(const T* logits, int64_t V, int64_t ld, const dp_params_t* params,
+                                      dp_penalty_t pen, double* out) {
+  const int64_t row = blockIdx.x;
+  const dp_params_t p = params[row];
+  if (penalties_neutral(p)) return;
+  const int32_t len = pen.len[row];
+  for (int32_t j = threadIdx.x; j < len; j += blockDim.x) {
+    const int32_t id = pen.ids[row * pen.cap + j];
+    out[row * V + id] = ready_penalized(Elem<T>::get(logits + row * ld, id), pen.out_count[row * pen.cap + j], p);
+  }
+}
+
+// SyntheticSource.column (service.py:459-463): base + noise * Gumbel(u),
+// u keyed by (seed, DOMAIN_LOGITS, iteration, seq, v), clamped at 2^-60.
+template <typename T>
+__global__ void synth_kernel(const double* base, double noise, uint64_t seed, uint64_t iteration,
+                             const uint64_t* seq_ids, int64_t V, int64_t ld, const int32_t* perm, T* out) {
+  const int64_t row = blockIdx.y;
+  const uint64_t h0 = mix64(hash_prefix(seed, kDomainLogits, iteration) ^ seq_ids[row]);
+  for (int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; pos < V; pos += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t id = perm ? (int64_t)perm[pos] : pos;
+    double u = unit53(mix64(h0 ^ (uint64_t)id));
+    u = fmax(u, 8.673617379884035e-19);   // 2^-60
+    const double g = -log(-log(u));
+    const double z = base[id] + noise * g;
+    if constexpr (sizeof(T) == 4) {
+      out[row * ld + pos] = (float)z;
+    } else {
+      out[row * ld + pos] = __float2bfloat16_rn((float)z);
+    }
+  }
+}
+
+}  // namespace dp
+
+using namespace dp;
+
+cudaError_t dp_launch_uniforms(const dp_params_t* params, const uint64_t* seq_ids, int64_t B,
+                               uint64_t iteration, double* out, cudaStream_t st) {
+  uniforms_kernel<<<(unsigned)((B + 127) / 128), 128, 0, st>>>(params, seq_ids, B, iteration, out);
+  return cudaGetLastError();
+}
+cudaError_t dp_launch_penalty_update(const dp_penalty_t& pen, const int32_t* token, int64_t B,
+                                     uint8_t* flags, cudaStream_t st) {
+  penalty_update_kernel<<<(unsigned)((B + 7) / 8), 256, 0, st>>>(pen, token, B, flags);
+  return cudaGetLastError();
+}
+cudaError_t dp_launch_penalty_reset(const dp_penalty_t& pen, int64_t B, cudaStream_t st) {
+  penalty_reset_kernel<<<(unsigned)B, 128, 0, st>>>(pen, B);
+  return cudaGetLastError();
+}
+cudaError_t dp_launch_ready_rows(const void* logits, int dtype, int64_t B, int64_t V, int64_t ld,
+                                 const dp_params_t* params, const dp_penalty_t& pen, double* out,
+                                 cudaStream_t st) {
+  dim3 g((unsigned)((V + 255) / 256 < 64 ? (V + 255) / 256 : 64), (unsigned)B);
+  if (dtype == DP_F32) {
+    ready_rows_kernel<float><<<g, 256, 0, st>>>((const float*)logits, V, ld, params, pen, out);
+    ready_rows_pen_kernel<float><<<(unsigned)B, 128, 0, st>>>((const float*)logits, V, ld, params, pen, out);
+  } else {
+    ready_rows_kernel<__nv_bfloat16><<<g, 256, 0, st>>>((const __nv_bfloat16*)logits, V, ld, params, pen, out);
+    ready_rows_pen_kernel<__nv_bfloat16><<<(unsigned)B, 128, 0, st>>>((const __nv_bfloat16*)logits, V, ld, params,
+                                                                        pen, out);
+  }
+  return cudaGetLastError();
+}
+cudaError_t dp_launch_synth(const double* base, double noise, uint64_t seed, uint64_t iteration,
+                            const uint64_t* seq_ids, int64_t B, int64_t V, int64_t ld, const int32_t* perm,
+                            int dtype, void* out, cudaStream_t st) {
+  dim3 g((unsigned)((V + 255) / 256 < 148 ? (V + 255) / 256 : 148), (unsigned)B);
+  if (dtype == DP_F32)
+    synth_kernel<float><<<g, 256, 0, st>>>(base, noise, seed, iteration, seq_ids, V, ld, perm, (float*)out);
+  else
+    synth_kernel<__nv_bfloat16><<<g, 256, 0, st>>>(base, noise, seed, iteration, seq_ids, V, ld, perm,
+                                                   (__nv_bfloat16*)out);
+  return cudaGetLastError();
+}

@@ -1,0 +1,260 @@
+// capi.cu — the extern "C" boundary (include/decplane_b200.h).  Argument
+// validation, launch planning and error mapping live here; kernels live in
+// sample_topk.cu / sample_general.cu / aux_kernels.cu.
+#include <cstdio>
+#include <cstring>
+
+#include "sampler.cuh"
+
+namespace dp {
+cudaError_t launch_topk(const SampleArgs& a, int dtype, int mode, int grid_rows, cudaStream_t st);
+cudaError_t launch_general(const SampleArgs& a, int dtype, int mode, int grid_rows, cudaStream_t st);
+cudaError_t launch_row_summary(const void* logits, int dtype, int64_t B, int64_t V, int64_t ld,
+                               const dp_params_t* params, const dp_penalty_t& pen, const int32_t* inv_perm,
+                               double* row_max, double* total, cudaStream_t st);
+cudaError_t launch_hot_mass_curve(const void* logits, int dtype, int64_t B, int64_t V, int64_t ld,
+                                  const double* row_max, const double* total, const dp_params_t* params,
+                                  const dp_penalty_t& pen, const int32_t* inv_perm, const int32_t* grid,
+                                  int32_t n_grid, double* out, cudaStream_t st);
+}  // namespace dp
+
+cudaError_t dp_launch_uniforms(const dp_params_t*, const uint64_t*, int64_t, uint64_t, double*, cudaStream_t);
+cudaError_t dp_launch_penalty_update(const dp_penalty_t&, const int32_t*, int64_t, uint8_t*, cudaStream_t);
+cudaError_t dp_launch_penalty_reset(const dp_penalty_t&, int64_t, cudaStream_t);
+cudaError_t dp_launch_ready_rows(const void*, int, int64_t, int64_t, int64_t, const dp_params_t*,
+                                 const dp_penalty_t&, double*, cudaStream_t);
+cudaError_t dp_launch_synth(const double*, double, uint64_t, uint64_t, const uint64_t*, int64_t, int64_t,
+                            int64_t, const int32_t*, int, void*, cudaStream_t);
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+int fail(int code, const char* fmt, const char* detail = nullptr) {
+  std::snprintf(g_err, sizeof(g_err), fmt, detail ? detail : "");
+  return code;
+}
+int cuda_status(cudaError_t e, const char* where) {
+  if (e == cudaSuccess) return DP_OK;
+  std::snprintf(g_err, sizeof(g_err), "%s: %s", where, cudaGetErrorString(e));
+  return DP_ERR_CUDA;
+}
+int sm_count() {
+  int dev = 0, n = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+uint32_t pow2_at_least(uint32_t v) {
+  uint32_t p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+bool valid_pen(const dp_penalty_t* pen, int64_t V) {
+  return pen && pen->ids && pen->out_count && pen->len && pen->cap >= 0 && pen->vocab_size == V;
+}
+
+// capacities for the streaming top-k kernel (see sample_topk.cu)
+void plan_topk(dp::SampleArgs& a, const dp_plan_t* plan, int64_t B, int64_t n, int elem_bytes) {
+  const int32_t kmax = (plan && plan->max_top_k > 0) ? plan->max_top_k : 256;
+  const uint32_t kcap = pow2_at_least((uint32_t)kmax + (uint32_t)a.pen.cap);
+  a.kcap = (int32_t)(kcap < 32u ? 32u : kcap);
+  if (a.kcap > 2048) a.kcap = 2048;
+  a.wcap = (int32_t)pow2_at_least((uint32_t)a.kcap + 160u);
+  a.lcap = (int32_t)pow2_at_least((uint32_t)kmax + 2u * (uint32_t)a.pen.cap + 1u);
+  if (a.lcap > 4096) a.lcap = 4096;
+  int split = plan && plan->split > 0 ? plan->split : 0;
+  if (split == 0) {
+    // aim for >= ~6 waves of 4 CTAs/SM, but keep >= 16K elements per CTA
+    const int64_t target = 6ll * 4 * sm_count();
+    split = (int)((target + B - 1) / B);
+    const int64_t by_len = n / 16384;
+    if (split > by_len) split = (int)by_len;
+    if (split < 1) split = 1;
+  }
+  if (split > 8) split = 8;
+  a.split = split;
+  (void)elem_bytes;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dp_version(void) { return 100; }
+
+const char* dp_last_error(void) { return g_err; }
+
+int dp_device_check(int device) {
+  cudaDeviceProp prop;
+  cudaError_t e = cudaGetDeviceProperties(&prop, device);
+  if (e != cudaSuccess) return cuda_status(e, "cudaGetDeviceProperties");
+  if (prop.major != 10) {
+    std::snprintf(g_err, sizeof(g_err), "device %d is sm_%d%d; this build targets sm_100a", device, prop.major,
+                  prop.minor);
+    return DP_ERR_UNSUPPORTED;
+  }
+  return DP_OK;
+}
+
+int dp_uniforms(const dp_params_t* params, const uint64_t* seq_ids, int64_t B, uint64_t iteration, double* out,
+                void* stream) {
+  if (!params || !seq_ids || !out || B < 0) return fail(DP_ERR_ARG, "dp_uniforms: null argument%s");
+  if (B == 0) return DP_OK;
+  return cuda_status(dp_launch_uniforms(params, seq_ids, B, iteration, out, (cudaStream_t)stream), "dp_uniforms");
+}
+
+int dp_sample_full(const void* logits, int dtype, int64_t B, int64_t V, int64_t ld, const dp_params_t* params,
+                   const dp_penalty_t* pen_host, const double* uniforms, const uint64_t* seq_ids,
+                   uint64_t iteration, int32_t* token, double* logprob, uint8_t* flags,
+                   const dp_debug_t* debug_host, const dp_plan_t* plan_host, void* stream) {
+  if (!logits || !params || !token || !logprob || !flags) return fail(DP_ERR_ARG, "dp_sample_full: null argument%s");
+  if (!uniforms && !seq_ids) return fail(DP_ERR_ARG, "dp_sample_full: need uniforms or seq_ids%s");
+  if (dtype != DP_F32 && dtype != DP_BF16) return fail(DP_ERR_UNSUPPORTED, "dp_sample_full: dtype%s");
+  if (B < 0 || V < 1 || ld < V || V >= (1ll << 31)) return fail(DP_ERR_ARG, "dp_sample_full: bad shape%s");
+  if (!valid_pen(pen_host, V)) return fail(DP_ERR_ARG, "dp_sample_full: penalty state does not match V%s");
+  if (B == 0) return DP_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  dp::SampleArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.logits = logits;
+  a.ld = ld;
+  a.V = V;
+  a.H = V;
+  a.params = params;
+  a.pen = *pen_host;
+  a.uniforms = uniforms;
+  a.seq_ids = seq_ids;
+  a.iteration = iteration;
+  a.n_rows = (int32_t)B;
+  a.token = token;
+  a.logprob = logprob;
+  a.flags = flags;
+  if (debug_host) a.dbg = *debug_host;
+  plan_topk(a, plan_host, B, V, dtype == DP_F32 ? 4 : 2);
+  cudaError_t e = dp::launch_topk(a, dtype, dp::kFull, (int)B, st);
+  if (e != cudaSuccess) return cuda_status(e, "dp_sample_full/topk");
+  e = dp::launch_general(a, dtype, dp::kFull, (int)B, st);
+  return cuda_status(e, "dp_sample_full/general");
+}
+
+int dp_row_summary(const void* logits, int dtype, int64_t B, int64_t V, int64_t ld, const dp_params_t* params,
+                   const dp_penalty_t* pen_host, const int32_t* inv_perm, double* row_max, double* total_expsum,
+                   void* stream) {
+  if (!logits || !params || !row_max || !total_expsum) return fail(DP_ERR_ARG, "dp_row_summary: null argument%s");
+  if (dtype != DP_F32 && dtype != DP_BF16) return fail(DP_ERR_UNSUPPORTED, "dp_row_summary: dtype%s");
+  if (B < 0 || V < 1 || ld < V) return fail(DP_ERR_ARG, "dp_row_summary: bad shape%s");
+  if (!valid_pen(pen_host, V)) return fail(DP_ERR_ARG, "dp_row_summary: penalty state does not match V%s");
+  if (B == 0) return DP_OK;
+  return cuda_status(dp::launch_row_summary(logits, dtype, B, V, ld, params, *pen_host, inv_perm, row_max,
+                                            total_expsum, (cudaStream_t)stream),
+                     "dp_row_summary");
+}
+
+int dp_sample_shvs(const void* logits, int dtype, int64_t B, int64_t V, int64_t H, int64_t ld, const int32_t* perm,
+                   const int32_t* inv_perm, const double* row_max, const double* total_expsum,
+                   const dp_params_t* params, const dp_penalty_t* pen_host, const double* uniforms,
+                   const uint64_t* seq_ids, uint64_t iteration, int32_t* token, double* logprob, uint8_t* flags,
+                   const dp_debug_t* debug_host, const dp_plan_t* plan_host, int32_t* scratch_rows,
+                   void* stream) {
+  if (!logits || !params || !token || !logprob || !flags || !row_max || !total_expsum || !scratch_rows)
+    return fail(DP_ERR_ARG, "dp_sample_shvs: null argument%s");
+  if (!uniforms && !seq_ids) return fail(DP_ERR_ARG, "dp_sample_shvs: need uniforms or seq_ids%s");
+  if (dtype != DP_F32 && dtype != DP_BF16) return fail(DP_ERR_UNSUPPORTED, "dp_sample_shvs: dtype%s");
+  if (B < 0 || V < 1 || H < 1 || H > V || ld < V || V >= (1ll << 31))
+    return fail(DP_ERR_ARG, "dp_sample_shvs: bad shape (need 1 <= H <= V <= ld)%s");
+  if ((perm == nullptr) != (inv_perm == nullptr)) return fail(DP_ERR_ARG, "dp_sample_shvs: perm/inv_perm%s");
+  if (!valid_pen(pen_host, V)) return fail(DP_ERR_ARG, "dp_sample_shvs: penalty state does not match V%s");
+  if (B == 0) return DP_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  dp::SampleArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.logits = logits;
+  a.ld = ld;
+  a.V = V;
+  a.H = H;
+  a.perm = perm;
+  a.inv_perm = inv_perm;
+  a.params = params;
+  a.pen = *pen_host;
+  a.uniforms = uniforms;
+  a.seq_ids = seq_ids;
+  a.iteration = iteration;
+  a.row_max = row_max;
+  a.total_expsum = total_expsum;
+  a.n_rows = (int32_t)B;
+  a.token = token;
+  a.logprob = logprob;
+  a.flags = flags;
+  if (debug_host) a.dbg = *debug_host;
+  int32_t* rej_count = scratch_rows;
+  int32_t* rej_rows = scratch_rows + 1;
+  cudaError_t e = cudaMemsetAsync(rej_count, 0, sizeof(int32_t), st);
+  if (e != cudaSuccess) return cuda_status(e, "dp_sample_shvs/memset");
+  a.reject_rows = rej_rows;
+  a.reject_count = rej_count;
+  // hot pass over [0, H)
+  plan_topk(a, plan_host, B, H, dtype == DP_F32 ? 4 : 2);
+  e = dp::launch_topk(a, dtype, dp::kHot, (int)B, st);
+  if (e != cudaSuccess) return cuda_status(e, "dp_sample_shvs/hot-topk");
+  e = dp::launch_general(a, dtype, dp::kHot, (int)B, st);
+  if (e != cudaSuccess) return cuda_status(e, "dp_sample_shvs/hot-general");
+  if (H == V) return DP_OK;
+  // tail pass over [H, V) for the rows the hot pass rejected
+  dp::SampleArgs t = a;
+  t.rows = rej_rows;
+  t.row_count = rej_count;
+  t.reject_rows = nullptr;
+  t.reject_count = nullptr;
+  plan_topk(t, plan_host, B, V - H, dtype == DP_F32 ? 4 : 2);
+  e = dp::launch_topk(t, dtype, dp::kTail, (int)B, st);
+  if (e != cudaSuccess) return cuda_status(e, "dp_sample_shvs/tail-topk");
+  e = dp::launch_general(t, dtype, dp::kTail, (int)B, st);
+  return cuda_status(e, "dp_sample_shvs/tail-general");
+}
+
+int dp_penalty_update(const dp_penalty_t* pen_host, const int32_t* token, int64_t B, uint8_t* flags, void* stream) {
+  if (!pen_host || !token || !pen_host->ids || !pen_host->out_count || !pen_host->len)
+    return fail(DP_ERR_ARG, "dp_penalty_update: null argument%s");
+  if (B == 0) return DP_OK;
+  return cuda_status(dp_launch_penalty_update(*pen_host, token, B, flags, (cudaStream_t)stream), "dp_penalty_update");
+}
+
+int dp_penalty_reset(const dp_penalty_t* pen_host, int64_t B, void* stream) {
+  if (!pen_host || !pen_host->prompt_len || !pen_host->len) return fail(DP_ERR_ARG, "dp_penalty_reset: null%s");
+  if (B == 0) return DP_OK;
+  return cuda_status(dp_launch_penalty_reset(*pen_host, B, (cudaStream_t)stream), "dp_penalty_reset");
+}
+
+int dp_ready_rows(const void* logits, int dtype, int64_t B, int64_t V, int64_t ld, const dp_params_t* params,
+                  const dp_penalty_t* pen_host, double* out, void* stream) {
+  if (!logits || !params || !out) return fail(DP_ERR_ARG, "dp_ready_rows: null argument%s");
+  if (!valid_pen(pen_host, V)) return fail(DP_ERR_ARG, "dp_ready_rows: penalty state does not match V%s");
+  if (B == 0) return DP_OK;
+  return cuda_status(dp_launch_ready_rows(logits, dtype, B, V, ld, params, *pen_host, out, (cudaStream_t)stream),
+                     "dp_ready_rows");
+}
+
+int dp_synth_logits(const double* base_by_id, double noise, uint64_t seed, uint64_t iteration,
+                    const uint64_t* seq_ids, int64_t B, int64_t V, int64_t ld, const int32_t* perm, int dtype,
+                    void* out, void* stream) {
+  if (!base_by_id || !seq_ids || !out) return fail(DP_ERR_ARG, "dp_synth_logits: null argument%s");
+  if (dtype != DP_F32 && dtype != DP_BF16) return fail(DP_ERR_UNSUPPORTED, "dp_synth_logits: dtype%s");
+  if (B == 0) return DP_OK;
+  return cuda_status(dp_launch_synth(base_by_id, noise, seed, iteration, seq_ids, B, V, ld, perm, dtype, out,
+                                     (cudaStream_t)stream),
+                     "dp_synth_logits");
+}
+
+int dp_hot_mass_curve(const void* logits, int dtype, int64_t B, int64_t V, int64_t ld, const double* row_max,
+                      const double* total_expsum, const dp_params_t* params, const dp_penalty_t* pen_host,
+                      const int32_t* inv_perm, const int32_t* grid, int32_t n_grid, double* out, void* stream) {
+  if (!logits || !row_max || !total_expsum || !params || !grid || !out || n_grid < 1)
+    return fail(DP_ERR_ARG, "dp_hot_mass_curve: null argument%s");
+  if (!valid_pen(pen_host, V)) return fail(DP_ERR_ARG, "dp_hot_mass_curve: penalty state does not match V%s");
+  if (B == 0) return DP_OK;
+  return cuda_status(dp::launch_hot_mass_curve(logits, dtype, B, V, ld, row_max, total_expsum, params, *pen_host,
+                                               inv_perm, grid, n_grid, out, (cudaStream_t)stream),
+                     "dp_hot_mass_curve");
+}
+
+}  // extern "C"

@@ -1,0 +1,183 @@
+// common.cuh — shared device helpers for the sm_100a decision-plane kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "decplane_b200.h"
+
+#define DP_DEV __device__ __forceinline__
+
+namespace dp {
+
+constexpr int kWarp = 32;
+
+DP_DEV int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+DP_DEV int64_t max64(int64_t a, int64_t b) { return a > b ? a : b; }
+constexpr double kBoundaryEps = 1e-6;   // north-star tolerance on CDF / accept boundaries
+
+// ---------------------------------------------------------------------------
+// counter RNG — SplitMix64 chain of rng.py:39-57 (bit-exact: u64 integer ops)
+constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;
+constexpr uint64_t kMultA = 0xBF58476D1CE4E5B9ull;
+constexpr uint64_t kMultB = 0x94D049BB133111EBull;
+constexpr uint64_t kDomainSampler = 0;
+constexpr uint64_t kDomainLogits = 1;
+
+DP_DEV uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * kMultA;
+  z = (z ^ (z >> 27)) * kMultB;
+  return z ^ (z >> 31);
+}
+// absorption up to the iteration field (rng.py:80-83)
+DP_DEV uint64_t hash_prefix(uint64_t seed, uint64_t domain, uint64_t iteration) {
+  uint64_t h = mix64(seed ^ kGolden);
+  h = mix64(h ^ domain);
+  return mix64(h ^ iteration);
+}
+DP_DEV double unit53(uint64_t h) { return (double)(h >> 11) * (1.0 / 9007199254740992.0); }
+DP_DEV void row_uniforms(uint64_t seed, uint64_t iteration, uint64_t seq, double u[3]) {
+  uint64_t h = mix64(hash_prefix(seed, kDomainSampler, iteration) ^ seq);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) u[i] = unit53(mix64(h ^ (uint64_t)i));
+}
+
+// ---------------------------------------------------------------------------
+// order-preserving keys.  -0.0 and +0.0 compare equal in the f64 oracle, so
+// both map to the +0 key; NaN is not a supported logit value.
+DP_DEV uint32_t f32_key(float x) {
+  uint32_t b = __float_as_uint(x);
+  if ((b << 1) == 0u) b = 0u;
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+DP_DEV float key_f32(uint32_t k) {
+  uint32_t b = (k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k;
+  return __uint_as_float(b);
+}
+DP_DEV uint64_t f64_key(double x) {
+  uint64_t b = (uint64_t)__double_as_longlong(x);
+  if ((b << 1) == 0ull) b = 0ull;
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+// composite selection key: value desc, position asc, unique per element
+DP_DEV uint64_t comp_key(float x, uint32_t pos) {
+  return ((uint64_t)f32_key(x) << 32) | (uint64_t)(0xFFFFFFFFu - pos);
+}
+DP_DEV uint32_t comp_pos(uint64_t k) { return 0xFFFFFFFFu - (uint32_t)(k & 0xFFFFFFFFull); }
+DP_DEV float comp_val(uint64_t k) { return key_f32((uint32_t)(k >> 32)); }
+
+// ---------------------------------------------------------------------------
+// element access
+template <typename T> struct Elem;
+template <> struct Elem<float> {
+  static constexpr int kPerVec = 4;   // 16-byte vector
+  DP_DEV static float get(const float* p, int64_t i) { return __ldg(p + i); }
+};
+template <> struct Elem<__nv_bfloat16> {
+  static constexpr int kPerVec = 8;
+  DP_DEV static float get(const __nv_bfloat16* p, int64_t i) {
+    unsigned short s = __ldg(reinterpret_cast<const unsigned short*>(p) + i);
+    return __uint_as_float(((uint32_t)s) << 16);
+  }
+};
+
+// 16-byte streaming load (read-once data: no L1 allocation)
+DP_DEV uint4 ld_stream16(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+template <typename T> DP_DEV float vec_elem(const uint4& v, int e);
+template <> DP_DEV float vec_elem<float>(const uint4& v, int e) {
+  uint32_t w = e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w;
+  return __uint_as_float(w);
+}
+template <> DP_DEV float vec_elem<__nv_bfloat16>(const uint4& v, int e) {
+  uint32_t w = (e >> 1) == 0 ? v.x : (e >> 1) == 1 ? v.y : (e >> 1) == 2 ? v.z : v.w;
+  return __uint_as_float((e & 1) ? (w & 0xFFFF0000u) : (w << 16));
+}
+
+// ---------------------------------------------------------------------------
+// penalties — penalty.py:35-78 + service.py:236-241, IEEE f64 op by op with
+// no FMA contraction so penalized values are bit-identical to numpy.
+DP_DEV bool penalties_neutral(const dp_params_t& p) {
+  return p.rep_penalty == 1.0 && p.presence_penalty == 0.0 && p.frequency_penalty == 0.0;
+}
+DP_DEV double ready_penalized(float x, int32_t out_count, const dp_params_t& p) {
+  double z = (double)x;
+  if (p.rep_penalty != 1.0) z = __ddiv_rn(z, p.rep_penalty);
+  if ((p.presence_penalty != 0.0 || p.frequency_penalty != 0.0) && out_count > 0) {
+    z = __dsub_rn(z, p.presence_penalty);
+    z = __dsub_rn(z, __dmul_rn(p.frequency_penalty, (double)out_count));
+  }
+  if (p.temperature != 1.0) z = __ddiv_rn(z, p.temperature);
+  return z;
+}
+DP_DEV double ready_plain(float x, const dp_params_t& p) {
+  double z = (double)x;
+  if (p.temperature != 1.0) z = __ddiv_rn(z, p.temperature);
+  return z;
+}
+
+// ---------------------------------------------------------------------------
+// warp helpers
+DP_DEV uint32_t lane_id() { return threadIdx.x & 31u; }
+DP_DEV uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+template <typename T> DP_DEV T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+template <typename T> DP_DEV T warp_max(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) { T w = __shfl_xor_sync(0xffffffffu, v, o); v = w > v ? w : v; }
+  return v;
+}
+// inclusive prefix sum across the warp
+template <typename T> DP_DEV T warp_incl_scan(T v) {
+  const int l = lane_id();
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T w = __shfl_up_sync(0xffffffffu, v, o);
+    if (l >= o) v += w;
+  }
+  return v;
+}
+
+// cluster helpers (sm_90+ ISA, used on sm_100a)
+DP_DEV uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+DP_DEV void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+DP_DEV void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+DP_DEV void cluster_sync() { cluster_arrive(); cluster_wait(); }
+// map a local shared address to the same offset in CTA `rank` of the cluster
+DP_DEV uint32_t dsmem_addr(const void* local, uint32_t rank) {
+  uint32_t a = (uint32_t)__cvta_generic_to_shared(local), r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+DP_DEV uint64_t ld_dsmem_u64(uint32_t addr) {
+  uint64_t v;
+  asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(addr));
+  return v;
+}
+DP_DEV uint32_t ld_dsmem_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+DP_DEV void atom_max_dsmem_u64(uint32_t addr, uint64_t v) {
+  asm volatile("atom.shared::cluster.max.u64 _, [%0], %1;" ::"r"(addr), "l"(v) : "memory");
+}
+
+}  // namespace dp

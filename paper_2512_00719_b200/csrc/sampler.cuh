@@ -1,0 +1,133 @@
+// sampler.cuh — shared per-row decision logic: domain description, penalty
+// entries, and the exact filter/draw over a sorted candidate list
+// (filtering.py:61-162 at tau_eff = 1).
+#pragma once
+
+#include "common.cuh"
+
+namespace dp {
+
+enum Mode : int { kFull = 0, kHot = 1, kTail = 2 };
+
+struct SampleArgs {
+  const void* logits;
+  int64_t ld, V, H;             // H = hot size (kHot/kTail), V for kFull
+  const int32_t* perm;          // position -> token id (NULL = identity)
+  const int32_t* inv_perm;      // token id -> position (NULL = identity)
+  const dp_params_t* params;
+  dp_penalty_t pen;
+  const double* uniforms;       // [B,3] or NULL (derive from seeds)
+  const uint64_t* seq_ids;
+  uint64_t iteration;
+  const double* row_max;        // producer summary (kHot)
+  const double* total_expsum;
+  int32_t* rows;                // row list (kTail: reject list) or NULL
+  int32_t* row_count;           // device count for `rows` (kTail) or NULL
+  int32_t n_rows;               // host row count when row_count == NULL
+  int32_t* token;
+  double* logprob;
+  uint8_t* flags;
+  dp_debug_t dbg;
+  int32_t* reject_rows;         // kHot: rows appended on rejection
+  int32_t* reject_count;
+  int32_t wcap, kcap, lcap, split;
+};
+
+DP_DEV int64_t dom_lo(const SampleArgs& a, int mode) { return mode == kTail ? a.H : 0; }
+DP_DEV int64_t dom_n(const SampleArgs& a, int mode) {
+  return mode == kFull ? a.V : (mode == kHot ? a.H : a.V - a.H);
+}
+DP_DEV int32_t pos_to_id(const SampleArgs& a, int64_t pos) {
+  return a.perm ? __ldg(a.perm + pos) : (int32_t)pos;
+}
+DP_DEV int64_t id_to_pos(const SampleArgs& a, int32_t id) {
+  return a.inv_perm ? (int64_t)__ldg(a.inv_perm + id) : (int64_t)id;
+}
+DP_DEV void get_uniforms(const SampleArgs& a, int row, const dp_params_t& p, double u[3]) {
+  if (a.uniforms) {
+    u[0] = a.uniforms[3 * (int64_t)row];
+    u[1] = a.uniforms[3 * (int64_t)row + 1];
+    u[2] = a.uniforms[3 * (int64_t)row + 2];
+  } else {
+    row_uniforms(p.seed, a.iteration, a.seq_ids[row], u);
+  }
+}
+// number of penalty entries that can change values for this row
+DP_DEV int32_t pen_len(const SampleArgs& a, int row, const dp_params_t& p) {
+  return penalties_neutral(p) ? 0 : a.pen.len[row];
+}
+
+// ---------------------------------------------------------------------------
+// Exact filter + inverse-CDF draw over candidates already sorted by
+// (ready desc, pos asc): _filter_core / filtered_draw / categorical_draw.
+// Executed by ONE warp.  r[0..n) ready values (f64, sorted), n >= 1;
+// `k` = number of candidates entering the top-p / min-p stages (the top-k
+// set, or the whole domain when top-k is off).  w / cum are scratch [n].
+struct DrawResult {
+  int32_t index;     // position in the sorted list
+  int32_t kept;
+  double logprob;
+  double margin;
+};
+
+DP_DEV DrawResult warp_filter_draw(const double* r, int32_t k, const dp_params_t& p, double u,
+                                   double* w, double* cum) {
+  const uint32_t lane = lane_id();
+  const double r0 = r[0];
+  // w_j = exp(r_j - r_0) (filtering.py:90), inclusive cumsum in f64
+  double carry = 0.0;
+  for (int32_t base = 0; base < k; base += 32) {
+    const int32_t j = base + lane;
+    const double wj = j < k ? exp(r[j] - r0) : 0.0;
+    const double c = warp_incl_scan(wj) + carry;
+    if (j < k) {
+      w[j] = wj;
+      cum[j] = c;
+    }
+    carry = __shfl_sync(0xffffffffu, c, 31);
+  }
+  __syncwarp();
+  int32_t kept = k;
+  double margin = 1e300;
+  if (p.top_p < 1.0) {                               // filtering.py:91-95
+    const double thr = p.top_p * cum[k - 1];
+    int32_t below = 0;
+    for (int32_t base = 0; base < k; base += 32) {
+      const int32_t j = base + lane;
+      below += __popc(__ballot_sync(0xffffffffu, j < k && cum[j] < thr));
+    }
+    const int32_t kp = below + 1;
+    kept = min(kept, kp);
+    for (int32_t j = max(0, kp - 2); j < min(k, kp + 1); ++j)
+      margin = fmin(margin, fabs(cum[j] - thr) / cum[k - 1]);
+  }
+  if (p.min_p > 0.0) {                               // filtering.py:96-98
+    const double floor_ = p.min_p * w[0];
+    int32_t ge = 0;
+    for (int32_t base = 0; base < k; base += 32) {
+      const int32_t j = base + lane;
+      ge += __popc(__ballot_sync(0xffffffffu, j < k && w[j] >= floor_));
+    }
+    kept = min(kept, ge);
+    for (int32_t j = max(0, ge - 1); j < min(k, ge + 1); ++j) margin = fmin(margin, fabs(w[j] - floor_));
+  }
+  kept = max(1, kept);                               // filtering.py:99
+  const double S = cum[kept - 1];
+  // j* = #(cdf_j <= u), clamped (filtering.py:158-162)
+  int32_t le = 0;
+  for (int32_t base = 0; base < kept; base += 32) {
+    const int32_t j = base + lane;
+    le += __popc(__ballot_sync(0xffffffffu, j < kept && cum[j] / S <= u));
+  }
+  const int32_t js = min(le, kept - 1);
+  margin = fmin(margin, fabs(cum[js] / S - u));
+  if (js > 0) margin = fmin(margin, fabs(cum[js - 1] / S - u));
+  DrawResult res;
+  res.index = js;
+  res.kept = kept;
+  res.logprob = log(w[js] / S);
+  res.margin = margin;
+  return res;
+}
+
+}  // namespace dp

@@ -1,0 +1,131 @@
+// select.cuh — exact radix selection on unique 64-bit composite keys
+// (value desc, position asc), the tie rule of _top_k_ids (filtering.py:38-58).
+//
+// Keys are unique (they embed the position), so "the `need` largest keys" is
+// a well-defined set and a most-significant-digit radix walk finds the cut in
+// at most 8 rounds of 8-bit digits, usually 2-4 because the walk stops as soon
+// as a whole digit bucket is selected.
+#pragma once
+
+#include "common.cuh"
+
+namespace dp {
+
+// Per-digit descending search over a 256-bin histogram, done by one warp.
+// Lane l owns bins 255-8l .. 248-8l.  Returns (digit, count strictly above
+// digit, count in digit) for the bucket where the running count reaches need.
+struct DigitHit {
+  uint32_t digit, above, inbin;
+};
+DP_DEV DigitHit warp_find_digit(const uint32_t* hist, uint32_t need) {
+  const uint32_t lane = lane_id();
+  uint32_t c[8], s = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    c[j] = hist[255 - 8 * lane - j];
+    s += c[j];
+  }
+  const uint32_t incl = warp_incl_scan(s);
+  const uint32_t excl = incl - s;
+  const uint32_t hit = __ballot_sync(0xffffffffu, excl < need && need <= incl);
+  const int L = __ffs(hit) - 1;
+  uint32_t d = 0, above = 0, inbin = 0;
+  if ((int)lane == L) {
+    uint32_t acc = excl;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (inbin == 0 && acc + c[j] >= need) {
+        d = 255 - 8 * lane - j;
+        above = acc;
+        inbin = c[j];
+      }
+      acc += c[j];
+    }
+  }
+  DigitHit r;
+  r.digit = __shfl_sync(0xffffffffu, d, L);
+  r.above = __shfl_sync(0xffffffffu, above, L);
+  r.inbin = __shfl_sync(0xffffffffu, inbin, L);
+  return r;
+}
+
+// Warp-level: threshold t such that exactly min(cnt, need) keys of buf[0,cnt)
+// are >= t.  hist: 256 u32 of warp-private shared memory.
+DP_DEV uint64_t warp_select_threshold(const uint64_t* buf, uint32_t cnt, uint32_t need,
+                                      uint32_t* hist) {
+  if (cnt <= need || need == 0) return need == 0 ? ~0ull : 0ull;
+  const uint32_t lane = lane_id();
+  uint64_t prefix = 0, mask = 0;
+  for (int shift = 56; shift >= 0; shift -= 8) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) hist[lane + 32 * i] = 0u;
+    __syncwarp();
+    for (uint32_t i = lane; i < cnt; i += 32) {
+      const uint64_t k = buf[i];
+      if ((k & mask) == prefix) atomicAdd(&hist[(uint32_t)(k >> shift) & 255u], 1u);
+    }
+    __syncwarp();
+    const DigitHit h = warp_find_digit(hist, need);
+    prefix |= (uint64_t)h.digit << shift;
+    mask |= 255ull << shift;
+    need -= h.above;
+    __syncwarp();
+    if (h.inbin == need) break;
+  }
+  return prefix;
+}
+
+// In-place stable compaction of buf[0,cnt) keeping keys >= t; returns new count.
+DP_DEV uint32_t warp_compact(uint64_t* buf, uint32_t cnt, uint64_t t) {
+  const uint32_t lane = lane_id();
+  uint32_t out = 0;
+  for (uint32_t base = 0; base < cnt; base += 32) {
+    const uint32_t i = base + lane;
+    const uint64_t k = i < cnt ? buf[i] : 0ull;
+    const bool keep = i < cnt && k >= t;
+    const uint32_t m = __ballot_sync(0xffffffffu, keep);
+    __syncwarp();
+    if (keep) buf[out + __popc(m & lanemask_lt())] = k;
+    out += __popc(m);
+    __syncwarp();
+  }
+  return out;
+}
+
+// Block-level threshold over an indexed source: get(i, &key) returns false for
+// empty slots, i in [0, n_slots).  hist: 256 u32 shared.  bcast: 4 u32 shared.
+// Every thread of the block must call it; returns the threshold to all.
+template <int NT, typename Get>
+DP_DEV uint64_t block_select_threshold(Get get, uint32_t n_slots, uint32_t cnt, uint32_t need,
+                                       uint32_t* hist, uint32_t* bcast) {
+  if (cnt <= need || need == 0) return need == 0 ? ~0ull : 0ull;
+  const uint32_t tid = threadIdx.x;
+  uint64_t prefix = 0, mask = 0;
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (uint32_t i = tid; i < 256; i += NT) hist[i] = 0u;
+    __syncthreads();
+    for (uint32_t i = tid; i < n_slots; i += NT) {
+      uint64_t k;
+      if (get(i, k) && (k & mask) == prefix) atomicAdd(&hist[(uint32_t)(k >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    if (tid < 32) {
+      const DigitHit h = warp_find_digit(hist, need);
+      if (tid == 0) {
+        bcast[0] = h.digit;
+        bcast[1] = h.above;
+        bcast[2] = h.inbin;
+      }
+    }
+    __syncthreads();
+    const uint32_t d = bcast[0], above = bcast[1], inbin = bcast[2];
+    prefix |= (uint64_t)d << shift;
+    mask |= 255ull << shift;
+    need -= above;
+    __syncthreads();
+    if (inbin == need) break;
+  }
+  return prefix;
+}
+
+}  // namespace dp

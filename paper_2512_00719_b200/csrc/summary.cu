@@ -1,0 +1,225 @@
+// summary.cu — producer row summary (K2) and the hot-mass curve (K6).
+//
+// K2 is make_shard_blocks' per-row (row_max, total_expsum) over the penalized,
+// temperature-scaled row (service.py:470-504, shvs.row_summary shvs.py:157-168):
+// one streaming pass with a per-thread online (max, sum) pair; penalized ids
+// are excluded from the stream through a shared-memory bitmap and added back
+// exactly in f64, so heavy penalties cannot cancel catastrophically.
+#include "sampler.cuh"
+
+namespace dp {
+
+template <int NT>
+DP_DEV double block_sum_f64(double v, double* red) {
+  v = warp_sum(v);
+  if ((threadIdx.x & 31u) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0) {
+    for (int w = 0; w < NT / 32; ++w) s += red[w];   // fixed order: deterministic
+    red[32] = s;
+  }
+  __syncthreads();
+  s = red[32];
+  __syncthreads();
+  return s;
+}
+template <int NT>
+DP_DEV float block_max_f32(float v, float* red) {
+  v = warp_max(v);
+  if ((threadIdx.x & 31u) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float m = red[0];
+    for (int w = 1; w < NT / 32; ++w) m = fmaxf(m, red[w]);
+    red[32] = m;
+  }
+  __syncthreads();
+  v = red[32];
+  __syncthreads();
+  return v;
+}
+
+template <typename T, int NT, int U>
+__global__ void __launch_bounds__(NT) row_summary_kernel(const T* logits, int64_t V, int64_t ld,
+                                                         const dp_params_t* params, dp_penalty_t pen,
+                                                         const int32_t* inv_perm, double* row_max,
+                                                         double* total) {
+  constexpr int EPV = Elem<T>::kPerVec;
+  extern __shared__ __align__(16) uint8_t smem[];
+  double* redd = reinterpret_cast<double*>(smem);
+  float* redf = reinterpret_cast<float*>(smem + 40 * 8);
+  uint32_t* bitmap = reinterpret_cast<uint32_t*>(smem + 40 * 8 + 40 * 4);
+  const int64_t row = blockIdx.x;
+  const dp_params_t p = params[row];
+  const T* x = logits + row * ld;
+  const int32_t plen = penalties_neutral(p) ? 0 : pen.len[row];
+  const int32_t* pids = pen.ids + row * pen.cap;
+  const int32_t* pcnt = pen.out_count + row * pen.cap;
+  const uint32_t words = plen > 0 ? (uint32_t)((V + 31) / 32) : 0u;
+  for (uint32_t i = threadIdx.x; i < words; i += NT) bitmap[i] = 0u;
+  __syncthreads();
+  for (int32_t j = threadIdx.x; j < plen; j += NT) {
+    const int64_t pos = inv_perm ? inv_perm[pids[j]] : pids[j];
+    atomicOr(&bitmap[pos >> 5], 1u << (pos & 31));
+  }
+  __syncthreads();
+  const float inv_tau = (float)(1.0 / p.temperature);
+  float m = -INFINITY;
+  double s = 0.0;
+  auto take = [&](float v, int64_t pos, bool valid) {
+    if (!valid) return;
+    if (plen > 0 && ((bitmap[pos >> 5] >> (pos & 31)) & 1u)) return;
+    if (v > m) {
+      s = (m == -INFINITY) ? 0.0 : s * (double)__expf((m - v) * inv_tau);
+      m = v;
+    }
+    s += (double)__expf((v - m) * inv_tau);
+  };
+  const uintptr_t addr = reinterpret_cast<uintptr_t>(x);
+  const int64_t a0 = min64(V, (int64_t)(((16u - (addr & 15u)) & 15u) / sizeof(T)));
+  const int64_t nvec = (V - a0) / EPV;
+  const int64_t tail0 = a0 + nvec * EPV;
+  if (threadIdx.x < 32) {
+    const int64_t i = threadIdx.x, ti = tail0 + threadIdx.x;
+    take(i < a0 ? Elem<T>::get(x, i) : 0.f, i, i < a0);
+    take(ti < V ? Elem<T>::get(x, ti) : 0.f, ti, ti < V);
+  }
+  const uint4* vp = reinterpret_cast<const uint4*>(x + a0);
+  for (int64_t base = threadIdx.x; base < nvec; base += (int64_t)NT * U) {
+    uint4 v[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const int64_t idx = base + (int64_t)j * NT;
+      v[j] = idx < nvec ? ld_stream16(vp + idx) : make_uint4(0u, 0u, 0u, 0u);
+    }
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const int64_t idx = base + (int64_t)j * NT;
+#pragma unroll
+      for (int e = 0; e < EPV; ++e) take(vec_elem<T>(v[j], e), a0 + idx * EPV + e, idx < nvec);
+    }
+  }
+  // combine thread states: global raw max, then rescale partial sums (f64)
+  const float mnp = block_max_f32<NT>(m, redf);
+  double sc = 0.0;
+  if (m != -INFINITY) sc = s * exp(((double)m - (double)mnp) * (double)inv_tau);
+  const double snp = block_sum_f64<NT>(sc, redd);
+  // penalized ids, exact f64 (penalty.py:66-78)
+  double rmax_pen = -INFINITY;
+  for (int32_t j = threadIdx.x; j < plen; j += NT) {
+    const int64_t pos = inv_perm ? inv_perm[pids[j]] : pids[j];
+    rmax_pen = fmax(rmax_pen, ready_penalized(Elem<T>::get(x, pos), pcnt[j], p));
+  }
+  rmax_pen = warp_max(rmax_pen);
+  if ((threadIdx.x & 31u) == 0) redd[threadIdx.x >> 5] = rmax_pen;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double mm = redd[0];
+    for (int w = 1; w < NT / 32; ++w) mm = fmax(mm, redd[w]);
+    redd[33] = mm;
+  }
+  __syncthreads();
+  const double rpen = redd[33];
+  __syncthreads();
+  const double rnp = mnp == -INFINITY ? -INFINITY : ready_plain(mnp, p);
+  const double M = fmax(rnp, rpen);
+  double spen = 0.0;
+  for (int32_t j = threadIdx.x; j < plen; j += NT) {
+    const int64_t pos = inv_perm ? inv_perm[pids[j]] : pids[j];
+    spen += exp(ready_penalized(Elem<T>::get(x, pos), pcnt[j], p) - M);
+  }
+  const double sp = block_sum_f64<NT>(spen, redd);
+  if (threadIdx.x == 0) {
+    row_max[row] = M;
+    total[row] = (rnp == -INFINITY ? 0.0 : snp * exp(rnp - M)) + sp;
+  }
+}
+
+// K6: out[row, g] = ready mass of hot positions [0, grid[g]) / total_expsum
+template <typename T, int NT>
+__global__ void __launch_bounds__(NT) hot_mass_curve_kernel(const T* logits, int64_t V, int64_t ld,
+                                                            const double* row_max, const double* total,
+                                                            const dp_params_t* params, dp_penalty_t pen,
+                                                            const int32_t* inv_perm, const int32_t* grid,
+                                                            int32_t n_grid, double* out) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  double* redd = reinterpret_cast<double*>(smem);
+  uint32_t* bitmap = reinterpret_cast<uint32_t*>(smem + 40 * 8);
+  const int64_t row = blockIdx.x;
+  const dp_params_t p = params[row];
+  const T* x = logits + row * ld;
+  const int32_t plen = penalties_neutral(p) ? 0 : pen.len[row];
+  const int32_t* pids = pen.ids + row * pen.cap;
+  const int32_t* pcnt = pen.out_count + row * pen.cap;
+  const int64_t hmax = grid[n_grid - 1];
+  const uint32_t words = plen > 0 ? (uint32_t)((hmax + 31) / 32) : 0u;
+  for (uint32_t i = threadIdx.x; i < words; i += NT) bitmap[i] = 0u;
+  __syncthreads();
+  for (int32_t j = threadIdx.x; j < plen; j += NT) {
+    const int64_t pos = inv_perm ? inv_perm[pids[j]] : pids[j];
+    if (pos < hmax) atomicOr(&bitmap[pos >> 5], 1u << (pos & 31));
+  }
+  __syncthreads();
+  const double M = row_max[row], S = total[row];
+  const double c = M * p.temperature;
+  const float c_hi = (float)c, c_lo = (float)(c - (double)(float)c);
+  const float inv_tau = (float)(1.0 / p.temperature);
+  double acc = 0.0;
+  int64_t lo = 0;
+  for (int32_t g = 0; g < n_grid; ++g) {
+    const int64_t hi = grid[g];
+    double s = 0.0;
+    for (int64_t pos = lo + threadIdx.x; pos < hi; pos += NT) {
+      if (plen > 0 && ((bitmap[pos >> 5] >> (pos & 31)) & 1u)) continue;
+      const float v = Elem<T>::get(x, pos);
+      s += (double)__expf(((v - c_hi) - c_lo) * inv_tau);
+    }
+    for (int32_t j = threadIdx.x; j < plen; j += NT) {
+      const int64_t pos = inv_perm ? inv_perm[pids[j]] : pids[j];
+      if (pos >= lo && pos < hi) s += exp(ready_penalized(Elem<T>::get(x, pos), pcnt[j], p) - M);
+    }
+    acc += block_sum_f64<NT>(s, redd);
+    if (threadIdx.x == 0) out[row * n_grid + g] = S > 0.0 ? fmin(acc / S, 1.0) : 0.0;
+    lo = hi;
+  }
+}
+
+cudaError_t launch_row_summary(const void* logits, int dtype, int64_t B, int64_t V, int64_t ld,
+                               const dp_params_t* params, const dp_penalty_t& pen, const int32_t* inv_perm,
+                               double* row_max, double* total, cudaStream_t st) {
+  constexpr int NT = 512, U = 4;
+  const size_t smem = 40 * 8 + 40 * 4 + (size_t)((V + 31) / 32) * 4;
+  if (dtype == DP_F32) {
+    auto k = row_summary_kernel<float, NT, U>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k<<<(unsigned)B, NT, smem, st>>>((const float*)logits, V, ld, params, pen, inv_perm, row_max, total);
+  } else {
+    auto k = row_summary_kernel<__nv_bfloat16, NT, U>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k<<<(unsigned)B, NT, smem, st>>>((const __nv_bfloat16*)logits, V, ld, params, pen, inv_perm, row_max, total);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_hot_mass_curve(const void* logits, int dtype, int64_t B, int64_t V, int64_t ld,
+                                  const double* row_max, const double* total, const dp_params_t* params,
+                                  const dp_penalty_t& pen, const int32_t* inv_perm, const int32_t* grid,
+                                  int32_t n_grid, double* out, cudaStream_t st) {
+  constexpr int NT = 256;
+  const size_t smem = 40 * 8 + (size_t)((V + 31) / 32) * 4;
+  if (dtype == DP_F32) {
+    auto k = hot_mass_curve_kernel<float, NT>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k<<<(unsigned)B, NT, smem, st>>>((const float*)logits, V, ld, row_max, total, params, pen, inv_perm, grid,
+                                     n_grid, out);
+  } else {
+    auto k = hot_mass_curve_kernel<__nv_bfloat16, NT>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k<<<(unsigned)B, NT, smem, st>>>((const __nv_bfloat16*)logits, V, ld, row_max, total, params, pen, inv_perm,
+                                     grid, n_grid, out);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace dp

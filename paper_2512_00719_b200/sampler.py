@@ -1,0 +1,264 @@
+"""Batched decision plane: logits [B, V] on the GPU -> next-token ids.
+
+`DecisionPlane.sample` is the B200 replacement for the reference's per-row
+worker loop (service.py:752-766: uniforms -> _Sampler.sample ->
+update_output_histogram) over a whole batch, in two or three kernel launches
+and no host synchronisation:
+
+* variant "full"  (service.py:381-409, _Sampler("offload-truncate")): fused
+  penalties -> /tau -> top-k -> top-p -> min-p -> inverse-CDF draw;
+* variant "shvs"  (service.py:354-380): hot prefix pass with the rejection
+  test against the producer summary (row_max, total_expsum), tail pass only
+  for rejected rows (on-device reject list).
+
+Per-row uniforms are keyed by (params.seed, iteration, seq_id) exactly as
+rng.pregenerate_slice (rng.py:94-113), so tokens are invariant to batching and
+to the GPU count.  The functional helpers `sample_full` / `shvs_sample` keep
+the reference signatures (filtering.py:172, shvs.py:258) for single rows.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .core import DegenerateRowError, SamplingParams, TokenDecision, params_bytes, validate_params
+from .penalty import PenaltyState
+from .shvs import HotVocab
+
+VARIANT_FULL = "full"
+VARIANT_SHVS = "shvs"
+
+
+def _dtype_code(t) -> int:
+    import torch
+
+    if t.dtype == torch.float32:
+        return N.DP_F32
+    if t.dtype == torch.bfloat16:
+        return N.DP_BF16
+    raise ValueError(f"logits dtype {t.dtype} unsupported (float32 or bfloat16)")
+
+
+def _ptr(t) -> C.c_void_p:
+    return C.c_void_p(0 if t is None else t.data_ptr())
+
+
+def _stream() -> C.c_void_p:
+    import torch
+
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+@dataclass
+class Decisions:
+    """Device-side results of one batched call (all tensors length B)."""
+
+    token: "object"          # int32
+    logprob: "object"        # float64
+    flags: "object"          # uint8
+    alpha: "object" = None   # float64 (SHVS hot mass)
+    margin: "object" = None  # float64 (closest decision-boundary distance)
+    kept: "object" = None
+    bytes_touched: "object" = None
+    topk_ids: "object" = None
+    topk_ready: "object" = None
+
+
+class DecisionPlane:
+    """A batch of B sequences with per-row params and GPU penalty state."""
+
+    def __init__(self, vocab_size: int, params, prompts=None, seq_ids=None, hot: HotVocab | None = None,
+                 device="cuda", max_generated: int = 256, pen_cap: int | None = None, split: int = 0):
+        import torch
+
+        self.device = torch.device(device)
+        N.require_device(self.device)
+        self.vocab_size = int(vocab_size)
+        params = list(params) if isinstance(params, (list, tuple)) else None if params is None else [params]
+        if prompts is None:
+            prompts = [[] for _ in range(len(params))]
+        self.batch = len(prompts)
+        if len(params) == 1 and self.batch > 1:
+            params = params * self.batch
+        self.seq_ids = np.arange(self.batch, dtype=np.uint64) if seq_ids is None else np.asarray(seq_ids, np.uint64)
+        if self.seq_ids.shape[0] != self.batch:
+            raise ValueError("seq_ids must have one entry per row")
+        self._seq_dev = torch.from_numpy(self.seq_ids.view(np.int64)).to(self.device)
+        self.state = PenaltyState(prompts, vocab_size, cap=pen_cap, device=self.device, max_generated=max_generated)
+        self.hot = hot
+        self.split = int(split)
+        self.set_params(params)
+        self._out = None
+        self._scratch = torch.empty(self.batch + 1, dtype=torch.int32, device=self.device)
+
+    # -- configuration -----------------------------------------------------
+    def set_params(self, params) -> None:
+        import torch
+
+        if len(params) != self.batch:
+            raise ValueError("need one SamplingParams per row")
+        for p in params:
+            errs = validate_params(p, self.vocab_size)
+            if errs:
+                raise ValueError("; ".join(errs))
+        self.params = list(params)
+        raw = np.frombuffer(params_bytes(self.params), dtype=np.uint8).copy()
+        self._params_dev = torch.from_numpy(raw).to(self.device)
+        ks = [p.top_k for p in self.params if p.top_k > 0]
+        self._plan = N.Plan(max(ks) if ks else 0, self.split)
+
+    def set_hot(self, hot: HotVocab | None) -> None:
+        """Hot-set changes land between iterations (service.py:602-610, :646-648)."""
+        self.hot = hot
+
+    @property
+    def params_dev(self):
+        return self._params_dev
+
+    def _outputs(self, debug: bool, topk_stride: int):
+        import torch
+
+        dev, b = self.device, self.batch
+        key = (debug, topk_stride)
+        if self._out is None or self._out[0] != key:
+            d = Decisions(torch.empty(b, dtype=torch.int32, device=dev), torch.empty(b, dtype=torch.float64, device=dev),
+                          torch.zeros(b, dtype=torch.uint8, device=dev))
+            d.alpha = torch.ones(b, dtype=torch.float64, device=dev)
+            if debug:
+                d.margin = torch.empty(b, dtype=torch.float64, device=dev)
+                d.kept = torch.empty(b, dtype=torch.int32, device=dev)
+                d.bytes_touched = torch.zeros(b, dtype=torch.int64, device=dev)
+                if topk_stride:
+                    d.topk_ids = torch.full((b, topk_stride), -1, dtype=torch.int32, device=dev)
+                    d.topk_ready = torch.full((b, topk_stride), float("nan"), dtype=torch.float64, device=dev)
+            self._out = (key, d)
+        return self._out[1]
+
+    def _debug_struct(self, d: Decisions, topk_stride: int, debug: bool) -> N.Debug:
+        if not debug:
+            return N.Debug(None, None, 0, 0, None, None, d.alpha.data_ptr(), None)
+        return N.Debug(_ptr(d.topk_ids).value, _ptr(d.topk_ready).value, topk_stride, 0, d.margin.data_ptr(),
+                       d.kept.data_ptr(), d.alpha.data_ptr(), d.bytes_touched.data_ptr())
+
+    # -- the hot path ----------------------------------------------------------
+    def sample(self, logits, iteration: int, variant: str = VARIANT_FULL, uniforms=None, summary=None,
+               update: bool = True, debug: bool = False, topk_stride: int = 0) -> Decisions:
+        """One decision per row.  `logits` is a [B, V] CUDA tensor (fp32/bf16,
+        unit stride along V) in vocab order for "full" and hot-first order for
+        "shvs".  `summary` = (row_max, total_expsum) f64 tensors from the
+        producer (make_shard_blocks contract, service.py:470-504); computed here
+        with one extra pass when omitted."""
+        if logits.dim() != 2 or logits.shape[0] != self.batch or logits.shape[1] != self.vocab_size:
+            raise ValueError(f"logits must be [{self.batch}, {self.vocab_size}]")
+        if not logits.is_cuda or logits.stride(1) != 1:
+            raise ValueError("logits must be a CUDA tensor with unit stride along the vocabulary")
+        dt = _dtype_code(logits)
+        d = self._outputs(debug, topk_stride)
+        dbg = self._debug_struct(d, topk_stride, debug)
+        st = _stream()
+        uni = _ptr(uniforms)
+        if variant == VARIANT_FULL:
+            N.call("dp_sample_full", _ptr(logits), dt, self.batch, self.vocab_size, logits.stride(0),
+                   _ptr(self._params_dev), C.byref(self.state.native), uni, _ptr(self._seq_dev), int(iteration),
+                   _ptr(d.token), _ptr(d.logprob), _ptr(d.flags), C.byref(dbg), C.byref(self._plan), st)
+        elif variant == VARIANT_SHVS:
+            if self.hot is None:
+                raise ValueError("SHVS needs a HotVocab")
+            perm, inv = self.hot.device_maps(self.device)
+            if summary is None:
+                summary = self.row_summary(logits, inv_perm=inv)
+            rmax, tot = summary
+            N.call("dp_sample_shvs", _ptr(logits), dt, self.batch, self.vocab_size, self.hot.size,
+                   logits.stride(0), _ptr(perm), _ptr(inv), _ptr(rmax), _ptr(tot), _ptr(self._params_dev),
+                   C.byref(self.state.native), uni, _ptr(self._seq_dev), int(iteration), _ptr(d.token),
+                   _ptr(d.logprob), _ptr(d.flags), C.byref(dbg), C.byref(self._plan), _ptr(self._scratch), st)
+        else:
+            raise ValueError(f"unknown variant {variant!r}")
+        if update:
+            self.state.update(d.token, d.flags)
+        return d
+
+    def row_summary(self, logits, inv_perm=None):
+        """(row_max, total_expsum) of the ready rows (service.py:484-489)."""
+        import torch
+
+        rmax = torch.empty(self.batch, dtype=torch.float64, device=self.device)
+        tot = torch.empty(self.batch, dtype=torch.float64, device=self.device)
+        N.call("dp_row_summary", _ptr(logits), _dtype_code(logits), self.batch, self.vocab_size, logits.stride(0),
+               _ptr(self._params_dev), C.byref(self.state.native), _ptr(inv_perm), _ptr(rmax), _ptr(tot), _stream())
+        return rmax, tot
+
+    def uniforms(self, iteration: int):
+        """rng.pregenerate_slice for every row, [B,3] f64 on device (rng.py:94-113)."""
+        import torch
+
+        out = torch.empty((self.batch, 3), dtype=torch.float64, device=self.device)
+        N.call("dp_uniforms", _ptr(self._params_dev), _ptr(self._seq_dev), self.batch, int(iteration),
+               _ptr(out), _stream())
+        return out
+
+    def to_decisions(self, d: Decisions, iteration: int, eos_ids=frozenset(), raise_degenerate: bool = True):
+        """Host TokenDecision list (core.py:172-181); synchronises."""
+        tok = d.token.cpu().numpy()
+        lp = d.logprob.cpu().numpy()
+        fl = d.flags.cpu().numpy()
+        out = []
+        for b in range(self.batch):
+            if fl[b] & N.FLAG_DEGENERATE:
+                if raise_degenerate:
+                    raise DegenerateRowError(f"row {b} (seq {int(self.seq_ids[b])}) has no usable probability mass")
+                out.append(None)
+                continue
+            t = int(tok[b])
+            out.append(TokenDecision(int(iteration), int(self.seq_ids[b]), t, t in eos_ids,
+                                     bool(fl[b] & N.FLAG_ACCEPTED_HOT), float(lp[b])))
+        return out
+
+
+# ---------------------------------------------------------------------------
+# reference-shaped single-row helpers
+
+
+def _one_row(logits_row, prompt, generated, params: SamplingParams, draws, vocab_size=None):
+    import torch
+
+    row = torch.as_tensor(logits_row)
+    if row.dim() != 1:
+        raise ValueError("logits_row must be 1-D")
+    v = row.shape[0] if vocab_size is None else vocab_size
+    if row.dtype not in (torch.float32, torch.bfloat16):
+        row = row.to(torch.float32)
+    plane = DecisionPlane(v, [params], prompts=[prompt], max_generated=max(len(generated), 1) + 1)
+    for t in generated:
+        plane.state.update(torch.tensor([t], dtype=torch.int32, device=plane.device))
+    u = torch.as_tensor(np.asarray(draws, dtype=np.float64).reshape(1, -1)[:, :3], device=plane.device)
+    if u.shape[1] < 3:
+        u = torch.nn.functional.pad(u, (0, 3 - u.shape[1]))
+    return plane, row.to(plane.device).reshape(1, -1).contiguous(), u
+
+
+def sample_full(logits_row, state, params: SamplingParams, draws, iteration_id: int = 0,
+                eos_ids=frozenset()) -> TokenDecision:
+    """filtering.sample_full (filtering.py:172-201) on the GPU for one row.
+    `state` is a core.SequenceState (prompt + generated tokens)."""
+    plane, row, u = _one_row(logits_row, state.prompt_tokens, state.tokens, params, draws)
+    d = plane.sample(row, iteration_id, VARIANT_FULL, uniforms=u, update=False)
+    dec = plane.to_decisions(d, iteration_id, eos_ids)[0]
+    dec.seq_id = state.seq_id
+    return dec
+
+
+def shvs_sample(logits_row, hot: HotVocab, state, params: SamplingParams, draws, iteration_id: int = 0,
+                eos_ids=frozenset()) -> TokenDecision:
+    """shvs.shvs_sample (shvs.py:258-289) on the GPU for one vocab-order row."""
+    plane, row, u = _one_row(logits_row, state.prompt_tokens, state.tokens, params, draws)
+    plane.set_hot(hot)
+    hot_row = hot.to_hot_first(row).contiguous()
+    d = plane.sample(hot_row, iteration_id, VARIANT_SHVS, uniforms=u, update=False)
+    dec = plane.to_decisions(d, iteration_id, eos_ids)[0]
+    dec.seq_id = state.seq_id
+    return dec

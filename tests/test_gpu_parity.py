@@ -1,0 +1,214 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the CPU oracle
+on identical logits and uniforms.
+
+Bar (north star): tokens identical except rows whose oracle decision margin is
+within 1e-6 of a CDF / accept / top-p / min-p boundary (each exemption is
+logged); top-k index sets bit-exact; penalized ready values within 1e-5
+relative (they are in fact bit-exact f64); logprobs within 1e-9 absolute.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import decplane_oracle as O
+from tests.golden_cases import Case
+
+pytestmark = pytest.mark.gpu
+
+EPS = 1e-6
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+
+    import build
+
+    build.build()
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def plane_for(torch, vocab, params, prompts, hot_ids=None, max_generated=64, split=0):
+    from paper_2512_00719_b200 import DecisionPlane, HotVocab, SamplingParams
+
+    hot = HotVocab(vocab, hot_ids) if hot_ids is not None else None
+    sp = [SamplingParams(**vars(p)) for p in params]
+    return DecisionPlane(vocab, sp, prompts=prompts, hot=hot, device="cuda", max_generated=max_generated,
+                         split=split)
+
+
+def compare(tag, gpu_tok, gpu_lp, dec, exempt_log):
+    """tokens equal unless the oracle margin is < EPS; logprob within 1e-9."""
+    bad = []
+    for b, d in enumerate(dec):
+        if int(gpu_tok[b]) == d.token:
+            assert abs(float(gpu_lp[b]) - d.logprob) <= 1e-9 + 1e-9 * abs(d.logprob), (tag, b)
+            continue
+        if d.margin < EPS:
+            exempt_log.append((tag, b, d.margin))
+            continue
+        bad.append((b, int(gpu_tok[b]), d.token, d.margin))
+    assert not bad, f"{tag}: token mismatches outside the boundary band: {bad[:8]}"
+
+
+def run_golden(torch, name, variant):
+    case = Case(name)
+    params = case.params()
+    states = case.states()
+    plane = plane_for(torch, case.vocab, params, [case.prompts[b] for b in range(case.batch)],
+                      hot_ids=case.hot_ids)
+    exempt = []
+    for it in range(case.iters):
+        x = case.logits(it)
+        dec = O.sample_batch(x, states, params, list(range(case.batch)), it, path=case.path,
+                             hot_ids=case.hot_ids)
+        # oracle == reference run (pinned on CPU); the GPU must match both
+        np.testing.assert_array_equal([d.token for d in dec], case.tokens[it])
+        xt = torch.from_numpy(x).cuda()
+        if variant == "shvs":
+            xt = plane.hot.to_hot_first(xt).contiguous()
+        d = plane.sample(xt, it, variant=variant, debug=True)
+        tok, lp = d.token.cpu().numpy(), d.logprob.cpu().numpy()
+        compare(f"{name}/it{it}", tok, lp, dec, exempt)
+        fl = d.flags.cpu().numpy()
+        if variant == "shvs":
+            acc = (fl & 0x02) != 0
+            for b, dd in enumerate(dec):
+                if dd.margin >= EPS:
+                    assert acc[b] == dd.accepted_hot, (name, it, b)
+                    assert abs(d.alpha.cpu().numpy()[b] - dd.alpha) < 1e-6
+        # keep GPU penalty state identical to the oracle's even for exempt rows
+        if not np.array_equal(tok, [dd.token for dd in dec]):
+            for b, dd in enumerate(dec):
+                if tok[b] != dd.token:
+                    states[b] = None
+            pytest.skip(f"boundary-exempt rows diverge state: {exempt}")
+        # penalty state parity: GPU sparse lists == oracle touched set
+        rows = plane.state.rows()
+        for b in range(case.batch):
+            ids, cnt = rows[b]
+            want = dict(O.State.entries(states[b]))
+            assert dict(zip(ids.tolist(), cnt.tolist())) == want
+    if exempt:
+        print("boundary exemptions:", exempt)
+
+
+def test_uniforms_bit_exact(torch_cuda, golden_dir):
+    from paper_2512_00719_b200 import rng
+
+    u = rng.pregenerate_slice(42, 9, range(100, 140)).cpu().numpy()
+    np.testing.assert_array_equal(u, O.pregenerate_slice(42, 9, range(100, 140)))
+    import os
+
+    for line in open(os.path.join(golden_dir, "rng_probes.txt")):
+        seed, it, seq, idx, hexval = line.split()
+        got = rng.draw(rng.DrawKey(int(seed), int(it), int(seq), int(idx)))
+        assert got.hex() == hexval
+
+
+def test_synthetic_logits_match_oracle_generator(torch_cuda):
+    from paper_2512_00719_b200.synthetic import SyntheticSource
+
+    src = SyntheticSource(4096, seed=0, device="cuda")
+    x = src.generate(3, range(8)).cpu().numpy()
+    ref = O.Synthetic(4096).wire(3, range(8))
+    # same f64 formula; CUDA log vs numpy log may differ in the last f64 bit,
+    # which survives the f32 cast only at rounding ties
+    assert np.mean(x == ref) > 0.9999
+    np.testing.assert_allclose(x, ref, rtol=2e-7, atol=0)
+
+
+@pytest.mark.parametrize("name", ["c1_full", "c2_full"])
+def test_full_path_matches_reference_run(torch_cuda, name):
+    run_golden(torch_cuda, name, "full")
+
+
+@pytest.mark.parametrize("name", ["shvs_accept", "shvs_reject"])
+def test_shvs_topk_matches_reference_run(torch_cuda, name):
+    run_golden(torch_cuda, name, "shvs")
+
+
+def test_topk_sets_and_ready_values_exact(torch_cuda):
+    torch = torch_cuda
+    v, bsz, k = 32000, 64, 50
+    params = [O.Params(temperature=0.8, top_k=k, top_p=0.9, rep_penalty=1.1, presence_penalty=0.3,
+                       frequency_penalty=0.05, seed=b) for b in range(bsz)]
+    prompts = [np.random.default_rng(b).integers(0, v, 32) for b in range(bsz)]
+    states = [O.State.new(p, v) for p in prompts]
+    plane = plane_for(torch, v, params, prompts)
+    src = O.Synthetic(v)
+    for it in range(3):
+        x = src.wire(it, range(bsz))
+        d = plane.sample(torch.from_numpy(x).cuda(), it, debug=True, topk_stride=k)
+        ids = d.topk_ids.cpu().numpy()
+        ready = d.topk_ready.cpu().numpy()
+        for b in range(bsz):
+            r = O.ready_row(x[b], states[b], params[b])
+            want = O.top_k_ids(r, k)
+            order = np.lexsort((want, -r[want]))
+            np.testing.assert_array_equal(ids[b], want[order])          # set AND canonical order
+            np.testing.assert_array_equal(ready[b], r[want[order]])      # bit-exact f64
+        tok = d.token.cpu().numpy()
+        for b in range(bsz):
+            states[b].update(int(tok[b]))
+
+
+def test_penalized_ready_rows_bit_exact(torch_cuda):
+    torch = torch_cuda
+    from paper_2512_00719_b200.penalty import apply_penalties
+
+    v, bsz = 4096, 16
+    params = [O.Params(temperature=[0.7, 1.0, 1.3][b % 3], rep_penalty=[1.1, 0.9, 1.0, 2.0][b % 4],
+                       presence_penalty=[0.0, 0.5, -0.4][b % 3], frequency_penalty=[0.1, 0.0][b % 2])
+              for b in range(bsz)]
+    prompts = [np.random.default_rng(b).integers(0, v, 40) for b in range(bsz)]
+    plane = plane_for(torch, v, params, prompts)
+    states = [O.State.new(p, v) for p in prompts]
+    rs = np.random.default_rng(9)
+    for _ in range(30):
+        t = rs.integers(0, v, bsz).astype(np.int32)
+        plane.state.update(torch.from_numpy(t).cuda())
+        for b in range(bsz):
+            states[b].update(int(t[b]))
+    x = O.Synthetic(v).wire(0, range(bsz))
+    got = apply_penalties(torch.from_numpy(x).cuda(), plane.state, plane.params_dev, 0).cpu().numpy()
+    for b in range(bsz):
+        np.testing.assert_array_equal(got[b], O.ready_row(x[b], states[b], params[b]))
+
+
+def test_full_size_c2_properties_and_sampled_parity(torch_cuda):
+    """C2 at full size (V=152064, B=1024): every row through the GPU; a row
+    sample through the oracle; size-independent properties on all rows."""
+    torch = torch_cuda
+    from paper_2512_00719_b200.synthetic import SyntheticSource
+
+    v, bsz, k = 152064, 1024, 50
+    kw = dict(temperature=0.8, top_k=k, top_p=0.9, min_p=0.05, rep_penalty=1.1, presence_penalty=0.5,
+              frequency_penalty=0.1)
+    params = [O.Params(**kw, seed=0) for _ in range(bsz)]
+    prompts = [np.random.default_rng(b).integers(0, v, 32) for b in range(bsz)]
+    states = [O.State.new(p, v) for p in prompts]
+    plane = plane_for(torch, v, params, prompts, max_generated=16)
+    src = SyntheticSource(v, device="cuda")
+    check_rows = list(range(0, bsz, 37))
+    exempt = []
+    for it in range(2):
+        x = src.generate(it, range(bsz))
+        d = plane.sample(x, it, debug=True, topk_stride=k)
+        tok = d.token.cpu().numpy()
+        lp = d.logprob.cpu().numpy()
+        kept = d.kept.cpu().numpy()
+        ids = d.topk_ids.cpu().numpy()
+        fl = d.flags.cpu().numpy()
+        assert not (fl & 0x80).any()
+        assert (lp <= 0).all() and (kept >= 1).all() and (kept <= k).all()
+        assert all(tok[b] in ids[b, : kept[b]] for b in range(bsz))
+        xh = x[check_rows].cpu().numpy()
+        dec = [O.sample_full_row(xh[i], states[b], params[b], O.uniforms_per_row([0], it, [b])[0])
+               for i, b in enumerate(check_rows)]
+        compare(f"c2full/it{it}", tok[check_rows], lp[check_rows], dec, exempt)
+        for b in range(bsz):
+            states[b].update(int(tok[b]))
+    print("exemptions:", exempt)

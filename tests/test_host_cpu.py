@@ -1,0 +1,144 @@
+"""CPU-only tests: the C-ABI library builds and exports every declared symbol,
+and the host-side logic (params, hot vocab, partitioning, sizing) matches the
+reference semantics.  No kernel is launched here."""
+
+import json
+import os
+import re
+
+import numpy as np
+import pytest
+
+from oracle import decplane_oracle as O
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    import build
+
+    build.build()
+    from paper_2512_00719_b200 import _native as N
+
+    return N.load()
+
+
+def test_library_exports_every_header_symbol(lib):
+    header = open(os.path.join(ROOT, "include", "decplane_b200.h")).read()
+    declared = set(re.findall(r"^DP_API\s+[\w\s\*]+?\b(dp_\w+)\(", header, flags=re.M))
+    assert {"dp_sample_full", "dp_sample_shvs", "dp_row_summary", "dp_penalty_update"} <= declared
+    for name in declared:
+        assert hasattr(lib, name), name
+    from paper_2512_00719_b200 import _native as N
+
+    assert set(N.EXPORTS) == declared
+    assert lib.dp_version() >= 100
+
+
+def test_struct_layouts_match_header():
+    import ctypes as C
+
+    from paper_2512_00719_b200 import _native as N
+
+    assert C.sizeof(N.Params) == 64
+    assert N.Params.top_p.offset == 16 and N.Params.seed.offset == 56
+    assert C.sizeof(N.Penalty) == 40
+    assert C.sizeof(N.Plan) == 32
+
+
+def test_library_rejects_bad_arguments_without_gpu(lib):
+    # argument validation happens before any CUDA call
+    import ctypes as C
+
+    from paper_2512_00719_b200 import _native as N
+
+    st = lib.dp_sample_full(None, 0, 1, 10, 10, None, None, None, None, 0, None, None, None, None, None, None)
+    assert st == N.DP_ERR_ARG
+    assert b"null" in lib.dp_last_error()
+    pen = N.Penalty(1, 1, 1, 1, 4, 99)
+    st = lib.dp_sample_full(C.c_void_p(1), 0, 1, 10, 10, C.c_void_p(1), C.byref(pen), None, C.c_void_p(1), 0,
+                            C.c_void_p(1), C.c_void_p(1), C.c_void_p(1), None, None, None)
+    assert st == N.DP_ERR_ARG and b"penalty" in lib.dp_last_error()
+    st = lib.dp_sample_full(C.c_void_p(1), 5, 1, 10, 10, C.c_void_p(1), C.byref(pen), None, C.c_void_p(1), 0,
+                            C.c_void_p(1), C.c_void_p(1), C.c_void_p(1), None, None, None)
+    assert st == N.DP_ERR_UNSUPPORTED
+
+
+def test_product_package_never_imports_oracle():
+    pkg = os.path.join(ROOT, "paper_2512_00719_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith(".py"):
+                src = open(os.path.join(dirpath, f)).read()
+                assert "oracle" not in re.findall(r"^\s*(?:from|import)\s+(\w+)", src, flags=re.M), f
+
+
+def test_validate_params_mirrors_reference():
+    from paper_2512_00719_b200 import SamplingParams, validate_params
+
+    assert validate_params(SamplingParams(), 100) == []
+    assert validate_params(SamplingParams(temperature=0.0), 10) == ["temperature must be positive"]
+    assert validate_params(SamplingParams(top_k=11), 10) == ["top_k exceeds vocabulary"]
+    errs = validate_params(SamplingParams(temperature=-1, top_p=0, min_p=1, rep_penalty=0, seed=-1), 10)
+    assert len(errs) == 5
+    assert SamplingParams(top_k=5).filters_neutral(5) and not SamplingParams(top_k=4).filters_neutral(5)
+    assert SamplingParams().penalties_neutral()
+
+
+def test_hot_vocab_layout_and_reference_tie_rules():
+    from paper_2512_00719_b200 import HotVocab, build_hot_vocab
+
+    assert build_hot_vocab([(0, 5), (1, 1), (2, 9), (3, 1)], 2, 4).hot_ids.tolist() == [2, 0]
+    assert build_hot_vocab([(0, 1), (1, 1), (2, 1)], 2, 3).hot_ids.tolist() == [0, 1]
+    hv = HotVocab(10, [7, 2, 5])
+    assert hv.tail_ids.tolist() == [0, 1, 3, 4, 6, 8, 9]
+    assert hv.perm.tolist() == [7, 2, 5, 0, 1, 3, 4, 6, 8, 9]
+    assert (hv.perm[hv.inv_perm] == np.arange(10)).all()
+    assert hv.resize(2).hot_ids.tolist() == [7, 2]
+    with pytest.raises(ValueError):
+        HotVocab(4, [1, 1])
+
+
+def test_hot_vocab_trace_roundtrip(tmp_path):
+    from paper_2512_00719_b200 import build_hot_vocab, load_hot_vocab_trace, save_hot_vocab_trace
+
+    trace = [(3, 10), (1, 10), (0, 4), (2, 1)]
+    p = tmp_path / "hot.tsv"
+    save_hot_vocab_trace(p, trace)
+    back = load_hot_vocab_trace(p)
+    assert back == [(1, 10), (3, 10), (0, 4), (2, 1)]
+    assert build_hot_vocab(back, 3, 4).hot_ids.tolist() == [1, 3, 0]
+
+
+def test_partition_batch_matches_reference():
+    from paper_2512_00719_b200 import partition_batch
+
+    for b in (1, 7, 64, 1000, 8192):
+        for w in (1, 2, 3, 8):
+            assert partition_batch(b, w) == O.partition_batch(b, w)
+
+
+def test_sizing_matches_reference_golden(golden_dir):
+    from paper_2512_00719_b200 import sizing
+
+    spec = json.load(open(os.path.join(golden_dir, "spec_examples.json")))
+    s = spec["sizing"]
+    curve = sizing.HitRatioCurve(s["grid"], s["alpha_bar"])
+    pts = [(h, 8.55e-6 + 1.06e-8 * h) for h in (4096, 8192, 16384, 32768)]
+    c0, c, _ = sizing.fit_affine_cost(pts)
+    assert abs(c0 - s["c0"]) <= 1e-12 * abs(s["c0"]) + 1e-18 and abs(c - s["c"]) <= 1e-12 * s["c"]
+    model = sizing.SizingModel(c0, c, curve, 128256)
+    assert sizing.optimal_hot_size(model) == s["hot"]
+    assert sizing.expected_cost(4096, model) == pytest.approx(s["cost_4096"], rel=1e-12)
+    assert sizing.optimal_hot_size(model, cycle_budget=6e-4) == s["hot_budget"]
+    lin = sizing.HitRatioCurve([1.0, 1000.0], [0.001, 1.0])
+    assert sizing.optimal_hot_size(sizing.SizingModel(0.0, 1.0, lin, 1000)) == spec["sizing_linear"] == 500
+
+
+def test_synthetic_hot_ordering_matches_oracle():
+    from paper_2512_00719_b200.synthetic import hot_ordering
+
+    for v in (16, 2048, 32000):
+        np.testing.assert_array_equal(hot_ordering(0, v), O.synthetic_hot_ordering(0, v))
+        np.testing.assert_array_equal(hot_ordering(5, v), O.synthetic_hot_ordering(5, v))
