@@ -89,13 +89,16 @@ typedef struct {
   int32_t* kept;         /* [B] candidates surviving top-k/top-p/min-p                     */
   double*  alpha;        /* [B] SHVS hot mass alpha (shvs.py:148-154)                      */
   uint64_t* bytes_touched; /* [B] logits bytes streamed for the row (VisitCounter analogue) */
+  int64_t* stats;          /* [24] launch counters: 0 rows, 1 re-streams (estimate too high),
+                              2 re-streams (buffer overflow), 3 candidates admitted        */
 } dp_debug_t;
 
 /* Launch plan supplied by the host (nullable -> conservative defaults).
  * max_top_k: upper bound of top_k over the rows of the call (0 = unknown);
  * rows whose top-k stage does not fit the planned capacity take the general
  * (radix) path, so the bound only affects speed, never results.
- * split: CTAs per row cluster for the streaming kernels (0 = auto, <= 8). */
+ * split: CTAs per row cluster for the streaming kernels (0 = auto, <= 8;
+ *        -1 = the persistent warp-specialised TMA-ring kernel). */
 typedef struct {
   int32_t max_top_k;
   int32_t split;

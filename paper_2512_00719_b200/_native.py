@@ -60,7 +60,7 @@ class Debug(C.Structure):
     _fields_ = [
         ("topk_ids", C.c_void_p), ("topk_ready", C.c_void_p), ("topk_stride", C.c_int32),
         ("reserved", C.c_int32), ("margin", C.c_void_p), ("kept", C.c_void_p),
-        ("alpha", C.c_void_p), ("bytes_touched", C.c_void_p),
+        ("alpha", C.c_void_p), ("bytes_touched", C.c_void_p), ("stats", C.c_void_p),
     ]
 
 

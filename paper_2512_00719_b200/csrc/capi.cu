@@ -9,6 +9,7 @@
 namespace dp {
 cudaError_t launch_topk(const SampleArgs& a, int dtype, int mode, int grid_rows, cudaStream_t st);
 cudaError_t launch_general(const SampleArgs& a, int dtype, int mode, int grid_rows, cudaStream_t st);
+cudaError_t launch_stream(const SampleArgs& a, int dtype, int mode, int grid, int32_t* work, cudaStream_t st);
 cudaError_t launch_row_summary(const void* logits, int dtype, int64_t B, int64_t V, int64_t ld,
                                const dp_params_t* params, const dp_penalty_t& pen, const int32_t* inv_perm,
                                double* row_max, double* total, cudaStream_t st);
@@ -49,6 +50,32 @@ uint32_t pow2_at_least(uint32_t v) {
   while (p < v) p <<= 1;
   return p;
 }
+// per-device work counters of the persistent kernels (stream-ordered reuse;
+// concurrent calls on different streams of one device are not supported)
+int32_t* work_counter(int slot) {
+  static int32_t* g_work[64] = {nullptr};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  if (!g_work[dev]) {
+    if (cudaMalloc(&g_work[dev], 16 * sizeof(int32_t)) != cudaSuccess) return nullptr;
+  }
+  return g_work[dev] + slot;
+}
+// the persistent TMA-ring kernel is opt-in (plan->split == -1) until it beats
+// the per-row CTA kernel; see sample_stream.cu
+bool use_stream(int64_t B, const dp_plan_t* plan) {
+  return plan && plan->split == -1 && B >= sm_count();
+}
+cudaError_t launch_sampler(const dp::SampleArgs& a, int dtype, int mode, int64_t B, bool stream, int slot,
+                           cudaStream_t st) {
+  if (stream) {
+    int32_t* w = work_counter(slot);
+    if (!w) return cudaErrorMemoryAllocation;
+    const int64_t grid = B < (int64_t)sm_count() ? B : (int64_t)sm_count();   // one persistent CTA per SM
+    return dp::launch_stream(a, dtype, mode, (int)grid, w, st);
+  }
+  return dp::launch_topk(a, dtype, mode, (int)B, st);
+}
 bool valid_pen(const dp_penalty_t* pen, int64_t V) {
   return pen && pen->ids && pen->out_count && pen->len && pen->cap >= 0 && pen->vocab_size == V;
 }
@@ -59,14 +86,20 @@ void plan_topk(dp::SampleArgs& a, const dp_plan_t* plan, int64_t B, int64_t n, i
   const uint32_t kcap = pow2_at_least((uint32_t)kmax + (uint32_t)a.pen.cap);
   a.kcap = (int32_t)(kcap < 32u ? 32u : kcap);
   if (a.kcap > 2048) a.kcap = 2048;
-  a.wcap = (int32_t)pow2_at_least((uint32_t)a.kcap + 160u);
+  // vector slots of the streaming stage's candidate buffer (wcap field): the
+  // estimated threshold admits ~2-3 kp elements per segment; overflow is
+  // handled exactly (re-stream), so this only sizes the common case
+  a.wcap = (int32_t)(4u * (uint32_t)a.kcap > 1024u ? 4u * (uint32_t)a.kcap : 1024u);
+  if (a.wcap > 4096) a.wcap = 4096;
   a.lcap = (int32_t)pow2_at_least((uint32_t)kmax + 2u * (uint32_t)a.pen.cap + 1u);
   if (a.lcap > 4096) a.lcap = 4096;
   int split = plan && plan->split > 0 ? plan->split : 0;
   if (split == 0) {
-    // aim for >= ~6 waves of 4 CTAs/SM, but keep >= 16K elements per CTA
-    const int64_t target = 6ll * 4 * sm_count();
-    split = (int)((target + B - 1) / B);
+    // one CTA per row once the batch fills the GPU (measured fastest at
+    // V=152k, B=1024); small batches split rows over a cluster so every SM
+    // streams, keeping >= 16K elements per CTA
+    const int64_t sms = sm_count();
+    split = B >= sms ? 1 : (int)((2 * sms + B - 1) / B);
     const int64_t by_len = n / 16384;
     if (split > by_len) split = (int)by_len;
     if (split < 1) split = 1;
@@ -131,7 +164,9 @@ int dp_sample_full(const void* logits, int dtype, int64_t B, int64_t V, int64_t 
   a.flags = flags;
   if (debug_host) a.dbg = *debug_host;
   plan_topk(a, plan_host, B, V, dtype == DP_F32 ? 4 : 2);
-  cudaError_t e = dp::launch_topk(a, dtype, dp::kFull, (int)B, st);
+  const bool persistent = use_stream(B, plan_host);
+  if (persistent) a.split = 1;
+  cudaError_t e = launch_sampler(a, dtype, dp::kFull, B, persistent, 0, st);
   if (e != cudaSuccess) return cuda_status(e, "dp_sample_full/topk");
   e = dp::launch_general(a, dtype, dp::kFull, (int)B, st);
   return cuda_status(e, "dp_sample_full/general");
@@ -194,7 +229,9 @@ int dp_sample_shvs(const void* logits, int dtype, int64_t B, int64_t V, int64_t 
   a.reject_count = rej_count;
   // hot pass over [0, H)
   plan_topk(a, plan_host, B, H, dtype == DP_F32 ? 4 : 2);
-  e = dp::launch_topk(a, dtype, dp::kHot, (int)B, st);
+  const bool persistent = use_stream(B, plan_host);
+  if (persistent) a.split = 1;
+  e = launch_sampler(a, dtype, dp::kHot, B, persistent, 1, st);
   if (e != cudaSuccess) return cuda_status(e, "dp_sample_shvs/hot-topk");
   e = dp::launch_general(a, dtype, dp::kHot, (int)B, st);
   if (e != cudaSuccess) return cuda_status(e, "dp_sample_shvs/hot-general");
@@ -206,7 +243,8 @@ int dp_sample_shvs(const void* logits, int dtype, int64_t B, int64_t V, int64_t 
   t.reject_rows = nullptr;
   t.reject_count = nullptr;
   plan_topk(t, plan_host, B, V - H, dtype == DP_F32 ? 4 : 2);
-  e = dp::launch_topk(t, dtype, dp::kTail, (int)B, st);
+  if (persistent) t.split = 1;
+  e = launch_sampler(t, dtype, dp::kTail, B, persistent, 2, st);
   if (e != cudaSuccess) return cuda_status(e, "dp_sample_shvs/tail-topk");
   e = dp::launch_general(t, dtype, dp::kTail, (int)B, st);
   return cuda_status(e, "dp_sample_shvs/tail-general");

@@ -82,6 +82,15 @@ template <> struct Elem<__nv_bfloat16> {
   }
 };
 
+DP_DEV float to_f32(float x) { return x; }
+DP_DEV float to_f32(__nv_bfloat16 x) { return __bfloat162float(x); }
+
+template <typename T>
+DP_DEV uint4 neg_inf_vec() {
+  return sizeof(T) == 4 ? make_uint4(0xFF800000u, 0xFF800000u, 0xFF800000u, 0xFF800000u)
+                        : make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u);
+}
+
 // 16-byte streaming load (read-once data: no L1 allocation)
 DP_DEV uint4 ld_stream16(const void* p) {
   uint4 r;
@@ -176,8 +185,100 @@ DP_DEV uint32_t ld_dsmem_u32(uint32_t addr) {
   asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(addr));
   return v;
 }
-DP_DEV void atom_max_dsmem_u64(uint32_t addr, uint64_t v) {
-  asm volatile("atom.shared::cluster.max.u64 _, [%0], %1;" ::"r"(addr), "l"(v) : "memory");
+DP_DEV void st_dsmem_u64(uint32_t addr, uint64_t v) {
+  asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(addr), "l"(v) : "memory");
+}
+DP_DEV void st_dsmem_u32(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+DP_DEV void st_dsmem_f64(uint32_t addr, double v) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
+}
+
+// mbarrier helpers (local CTA barrier, remote arrive from cluster peers)
+DP_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)),
+               "r"(count) : "memory");
+}
+DP_DEV void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+// arrive on the barrier at a shared::cluster address (release at cluster scope)
+DP_DEV void mbar_remote_arrive(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+DP_DEV void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2, %3;\n"
+        " selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done) : "r"(a), "r"(parity), "r"(1000000u) : "memory");
+  }
+}
+
+DP_DEV void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((uint32_t)__cvta_generic_to_shared(bar)) : "memory");
+}
+DP_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(bar)),
+               "r"(bytes)
+               : "memory");
+}
+DP_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+  // suspend in hardware until the phase completes (or the hint expires)
+  // instead of re-polling: spinning warps would steal issue slots from the
+  // warps doing real work on the same SM sub-partition
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+        " selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done) : "r"(a), "r"(parity), "r"(1000000u) : "memory");
+  }
+}
+// 1-D TMA bulk copy global -> shared, completion counted on `bar` (bytes % 16 == 0)
+DP_DEV void tma_load_1d(void* dst_smem, const void* src_gmem, uint32_t bytes, uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          (uint32_t)__cvta_generic_to_shared(dst_smem)),
+      "l"(src_gmem), "r"(bytes), "r"((uint32_t)__cvta_generic_to_shared(bar)), "l"(policy)
+      : "memory");
+}
+DP_DEV uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+DP_DEV void named_bar_sync(uint32_t id, uint32_t nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+DP_DEV uint4 lds128(const void* p) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"((uint32_t)__cvta_generic_to_shared(p)));
+  return v;
+}
+
+// descending bitonic sort of one u32 key per lane across a warp
+DP_DEV uint32_t warp_sort_desc(uint32_t k) {
+  const uint32_t lane = lane_id();
+#pragma unroll
+  for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      const uint32_t o = __shfl_xor_sync(0xffffffffu, k, stride);
+      const bool lower = (lane & stride) == 0;
+      const bool desc = (lane & size) == 0 || size == 32;
+      const uint32_t hi = k > o ? k : o, lo = k > o ? o : k;
+      k = (lower == desc) ? hi : lo;
+    }
+  }
+  return k;
 }
 
 }  // namespace dp

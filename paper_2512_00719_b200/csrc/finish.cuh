@@ -1,0 +1,346 @@
+// finish.cuh — per-row final stage shared by the streaming samplers: exact
+// penalties on the sparse list (penalty.py:66-78), /tau (service.py:236-241),
+// canonical ordering (filtering.py:83), top-p / min-p / inverse-CDF draw
+// (filtering.py:61-162), and for SHVS the accept test (shvs.py:223-236).
+#pragma once
+
+#include "sampler.cuh"
+
+namespace dp {
+
+// shared-memory carve-up of the final stage
+struct FinLayout {
+  uint32_t key, r, w, cum, pos, hash, hash_cap, bytes;
+};
+__host__ __device__ inline FinLayout fin_layout(int lcap) {
+  FinLayout f;
+  f.hash_cap = 1;
+  while (f.hash_cap < 2u * (uint32_t)lcap) f.hash_cap <<= 1;
+  uint32_t o = 0;
+  f.key = o; o += lcap * 8u;
+  f.r = o; o += lcap * 8u;
+  f.w = o; o += lcap * 8u;
+  f.cum = o; o += lcap * 8u;
+  f.pos = o; o += lcap * 4u;
+  f.hash = o; o += f.hash_cap * 4u;
+  f.bytes = o;
+  return f;
+}
+
+struct FinishScratch {
+  uint32_t nl;
+  uint32_t pad;
+  double sh_pen[32];
+};
+
+// Penalty entries of a row whose loads are issued early (before the
+// selection) so their latency overlaps it: entries j = t + i*NT, i < 2.
+struct PenPrefetch {
+  float x[2];
+  int32_t cnt[2];
+  int32_t pos[2];   // domain position, -1 if absent / outside the domain
+};
+
+template <typename T, int NT>
+DP_DEV PenPrefetch pen_prefetch(const SampleArgs& a, int row, int32_t plen, const T* rowp, int64_t lo, int64_t n,
+                                uint32_t t) {
+  PenPrefetch pp;
+  const int32_t* pids = a.pen.ids + (int64_t)row * a.pen.cap;
+  const int32_t* pcnt = a.pen.out_count + (int64_t)row * a.pen.cap;
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int32_t j = (int32_t)t + i * NT;
+    pp.pos[i] = -1;
+    pp.x[i] = 0.f;
+    pp.cnt[i] = 0;
+    if (j < plen) {
+      const int64_t pos = id_to_pos(a, pids[j]) - lo;
+      if (pos >= 0 && pos < n) {
+        pp.pos[i] = (int32_t)pos;
+        pp.x[i] = Elem<T>::get(rowp, pos);
+        pp.cnt[i] = pcnt[j];
+      }
+    }
+  }
+  return pp;
+}
+
+// Descending bitonic sort of 32*E (u64 key, u32 pos) pairs held in registers
+// by one warp; element i = j*32 + lane lives in slot j of lane `lane`.
+// Order: key desc, pos asc (the canonical (value desc, id asc) rule).
+template <int E>
+DP_DEV void warp_reg_sort(uint64_t (&key)[E], uint32_t (&pos)[E]) {
+  const uint32_t lane = lane_id();
+  constexpr int N = 32 * E;
+#pragma unroll
+  for (int size = 2; size <= N; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      if (stride >= 32) {
+        const int js = stride / 32;
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+          if ((j & js) == 0) {
+            const int jp = j | js;
+            const uint32_t i = (uint32_t)j * 32u + lane;
+            const bool desc = (i & (uint32_t)size) == 0u;
+            const bool a_first = key[j] > key[jp] || (key[j] == key[jp] && pos[j] < pos[jp]);
+            if (a_first != desc) {
+              const uint64_t tk = key[j]; key[j] = key[jp]; key[jp] = tk;
+              const uint32_t tp = pos[j]; pos[j] = pos[jp]; pos[jp] = tp;
+            }
+          }
+        }
+      } else {
+        const bool lower = (lane & (uint32_t)stride) == 0u;
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+          const uint64_t ok = __shfl_xor_sync(0xffffffffu, key[j], stride);
+          const uint32_t op = __shfl_xor_sync(0xffffffffu, pos[j], stride);
+          const uint32_t i = (uint32_t)j * 32u + lane;
+          const bool desc = (i & (uint32_t)size) == 0u;
+          const bool mine_first = key[j] > ok || (key[j] == ok && pos[j] < op);
+          const bool keep_mine = (lower == desc) ? mine_first : !mine_first;
+          if (!keep_mine) {
+            key[j] = ok;
+            pos[j] = op;
+          }
+        }
+      }
+    }
+  }
+}
+
+template <int E>
+DP_DEV void warp_sort_regs(uint64_t* fkey, uint32_t* fpos) {
+  const uint32_t lane = lane_id();
+  uint64_t k[E];
+  uint32_t p[E];
+#pragma unroll
+  for (int j = 0; j < E; ++j) {
+    k[j] = fkey[j * 32 + lane];
+    p[j] = fpos[j * 32 + lane];
+  }
+  warp_reg_sort<E>(k, p);
+#pragma unroll
+  for (int j = 0; j < E; ++j) {
+    fkey[j * 32 + lane] = k[j];
+    fpos[j * 32 + lane] = p[j];
+  }
+  __syncwarp();
+}
+
+// Runs on NT cooperating threads (thread index `t`); `sync` is their barrier.
+// sel[0..nsel): unique (value desc, position asc) keys of the raw candidates.
+// `pp` holds the prefetched first 2*NT penalty entries.
+// Returns false when a kHot row was rejected (token left to the tail pass).
+template <typename T, int MODE, int NT, typename Sync>
+DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32_t plen, const T* rowp,
+                       int64_t lo, int64_t n, const uint64_t* sel, uint32_t nsel, double sh_unpen, double mrow,
+                       uint8_t* fin, const FinLayout& F, FinishScratch& fs, uint32_t t, Sync sync,
+                       const PenPrefetch* pp = nullptr) {
+  const uint32_t warp = t >> 5, lane = t & 31u;
+  const int32_t k = p.top_k;
+  const int32_t* pids = a.pen.ids + (int64_t)row * a.pen.cap;
+  const int32_t* pcnt = a.pen.out_count + (int64_t)row * a.pen.cap;
+  uint64_t* fkey = reinterpret_cast<uint64_t*>(fin + F.key);
+  double* fr = reinterpret_cast<double*>(fin + F.r);
+  double* fw = reinterpret_cast<double*>(fin + F.w);
+  double* fcum = reinterpret_cast<double*>(fin + F.cum);
+  uint32_t* fpos = reinterpret_cast<uint32_t*>(fin + F.pos);
+  uint32_t* hash = reinterpret_cast<uint32_t*>(fin + F.hash);
+  uint32_t hcap = 64;
+  while (hcap < 2u * (uint32_t)plen) hcap <<= 1;
+  if (hcap > F.hash_cap) hcap = F.hash_cap;
+  const uint32_t hmask = hcap - 1u;
+  double u[3];
+  get_uniforms(a, row, p, u);
+  const bool prof = a.dbg.stats != nullptr && t == 0;
+  long long pc = prof ? clock64() : 0;
+  auto lap = [&](int slot) {
+    if (prof) {
+      const long long now = clock64();
+      atomicAdd((unsigned long long*)&a.dbg.stats[slot], (unsigned long long)(now - pc));
+      pc = now;
+    }
+  };
+
+  // penalty entry e: (domain position, x, count), from the prefetch or memory
+  auto pen_entry = [&](int32_t j, int32_t& pos, float& x, int32_t& c) {
+    const int i = (j - (int32_t)t) / NT;
+    if (pp != nullptr && i < 2) {
+      pos = pp->pos[i];
+      x = pp->x[i];
+      c = pp->cnt[i];
+      return;
+    }
+    const int64_t q = id_to_pos(a, pids[j]) - lo;
+    pos = (q >= 0 && q < n) ? (int32_t)q : -1;
+    x = pos >= 0 ? Elem<T>::get(rowp, q) : 0.f;
+    c = pcnt[j];
+  };
+
+  // kHot: alpha and the accept test first (shvs.py:223-236)
+  double alpha = 1.0;
+  if (MODE == kHot) {
+    double spen = 0.0;   // exact mass of penalized hot ids (f64)
+    for (int32_t j = t; j < plen; j += NT) {
+      int32_t pos, c;
+      float x;
+      pen_entry(j, pos, x, c);
+      if (pos >= 0) spen += exp(ready_penalized(x, c, p) - mrow);
+    }
+    spen = warp_sum(spen);
+    if (lane == 0) fs.sh_pen[warp] = spen;
+    sync();
+    double sH = sh_unpen;
+    for (int w = 0; w < NT / 32; ++w) sH += fs.sh_pen[w];   // fixed order: deterministic
+    const double S = a.total_expsum[row];
+    const bool tail_empty = a.V == a.H;
+    bool degenerate = false;
+    if (!tail_empty) {
+      if (!(S > 0.0) || !isfinite(S)) degenerate = true;
+      else alpha = fmin(sH / S, 1.0);
+    }
+    const bool accept = !degenerate && sH > 0.0 && (tail_empty || u[1] <= alpha);
+    if (!accept) {
+      if (t == 0) {
+        uint8_t fl = DP_FLAG_REJECTED;
+        if (degenerate || (tail_empty && !(sH > 0.0))) fl |= DP_FLAG_DEGENERATE;
+        else if (fabs(u[1] - alpha) < kBoundaryEps) fl |= DP_FLAG_NEAR_BOUNDARY;
+        a.flags[row] = fl;
+        if (a.dbg.alpha) a.dbg.alpha[row] = alpha;
+        if (a.dbg.margin) a.dbg.margin[row] = fabs(u[1] - alpha);
+        if (a.dbg.bytes_touched) a.dbg.bytes_touched[row] = (uint64_t)n * sizeof(T);
+        if (!(fl & DP_FLAG_DEGENERATE)) {
+          a.reject_rows[atomicAdd(a.reject_count, 1)] = row;
+        } else {
+          a.token[row] = -1;
+          a.logprob[row] = 0.0;
+        }
+      }
+      sync();
+      return false;
+    }
+  }
+
+  // penalized positions of this domain -> hash set (raw candidates defer to them)
+  if (t == 0) fs.nl = 0u;
+  for (uint32_t i = t; i < hcap; i += NT) hash[i] = 0xFFFFFFFFu;
+  sync();
+  for (int32_t j = t; j < plen; j += NT) {
+    int32_t pos, c;
+    float x;
+    pen_entry(j, pos, x, c);
+    if (pos >= 0) {
+      uint32_t h = ((uint32_t)pos * 2654435761u) & hmask;
+      while (atomicCAS(&hash[h], 0xFFFFFFFFu, (uint32_t)pos) != 0xFFFFFFFFu) h = (h + 1u) & hmask;
+      const uint32_t s = atomicAdd(&fs.nl, 1u);
+      fkey[s] = f64_key(ready_penalized(x, c, p));
+      fpos[s] = (uint32_t)pos;
+    }
+  }
+  sync();
+  lap(12);
+  for (uint32_t i = t; i < nsel; i += NT) {
+    const uint64_t key = sel[i];
+    const uint32_t pos = comp_pos(key);
+    bool is_pen = false;
+    if (MODE != kHot && plen > 0) {
+      uint32_t h = (pos * 2654435761u) & hmask;
+      while (true) {
+        const uint32_t hv = hash[h];
+        if (hv == pos) { is_pen = true; break; }
+        if (hv == 0xFFFFFFFFu) break;
+        h = (h + 1u) & hmask;
+      }
+    }
+    if (!is_pen) {
+      const uint32_t s = atomicAdd(&fs.nl, 1u);
+      fkey[s] = f64_key(ready_plain(comp_val(key), p));
+      fpos[s] = pos;
+    }
+  }
+  sync();
+  const uint32_t nl = fs.nl;
+  uint32_t p2 = 128;
+  while (p2 < nl) p2 <<= 1;
+  for (uint32_t i = nl + t; i < p2; i += NT) {
+    fkey[i] = 0ull;
+    fpos[i] = 0xFFFFFFFFu;
+  }
+  sync();
+  lap(13);
+  // canonical order (ready desc, position asc): one warp through registers
+  // for short lists, all NT threads in shared memory otherwise
+  if (p2 <= 256) {
+    if (warp == 0) {
+      if (p2 <= 128) warp_sort_regs<4>(fkey, fpos);
+      else warp_sort_regs<8>(fkey, fpos);
+      const uint32_t m = min((uint32_t)k, nl);
+      for (uint32_t i = lane; i < m; i += 32) {
+        const uint64_t kk = fkey[i];
+        const uint64_t bb = (kk >> 63) ? (kk & 0x7FFFFFFFFFFFFFFFull) : ~kk;
+        fr[i] = __longlong_as_double((long long)bb);
+      }
+      __syncwarp();
+    }
+  } else {
+    for (uint32_t size = 2; size <= p2; size <<= 1)
+      for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+        for (uint32_t i = t; i < p2 / 2; i += NT) {
+          const uint32_t lo_i = 2 * stride * (i / stride) + (i % stride);
+          const uint32_t hi_i = lo_i + stride;
+          const bool desc = ((lo_i & size) == 0);
+          const uint64_t ka = fkey[lo_i], kb = fkey[hi_i];
+          const uint32_t pa = fpos[lo_i], pb = fpos[hi_i];
+          const bool a_first = ka > kb || (ka == kb && pa < pb);
+          if (a_first != desc) {
+            fkey[lo_i] = kb; fkey[hi_i] = ka;
+            fpos[lo_i] = pb; fpos[hi_i] = pa;
+          }
+        }
+        sync();
+      }
+    for (uint32_t i = t; i < nl; i += NT) {
+      const uint64_t kk = fkey[i];
+      const uint64_t bb = (kk >> 63) ? (kk & 0x7FFFFFFFFFFFFFFFull) : ~kk;
+      fr[i] = __longlong_as_double((long long)bb);
+    }
+    sync();
+  }
+
+  lap(14);
+  if (warp == 0) {
+    const DrawResult d = warp_filter_draw(fr, k, p, u[MODE == kTail ? 2 : 0], fw, fcum, a.dbg.stats);
+    lap(16);
+    if (lane == 0) {
+      const int64_t pos = (int64_t)fpos[d.index] + lo;
+      a.token[row] = pos_to_id(a, pos);
+      a.logprob[row] = d.logprob;
+      uint8_t fl = MODE == kHot ? DP_FLAG_ACCEPTED_HOT : (MODE == kTail ? DP_FLAG_REJECTED : 0);
+      double margin = d.margin;
+      if (MODE == kHot && a.V != a.H) margin = fmin(margin, fabs(u[1] - alpha));
+      if (margin < kBoundaryEps) fl |= DP_FLAG_NEAR_BOUNDARY;
+      if (MODE == kTail) fl |= a.flags[row] & DP_FLAG_NEAR_BOUNDARY;
+      a.flags[row] = fl;
+      if (a.dbg.margin) a.dbg.margin[row] = MODE == kTail ? fmin(margin, a.dbg.margin[row]) : margin;
+      if (a.dbg.kept) a.dbg.kept[row] = d.kept;
+      if (MODE == kHot && a.dbg.alpha) a.dbg.alpha[row] = alpha;
+      if (a.dbg.bytes_touched)
+        a.dbg.bytes_touched[row] = (MODE == kTail ? a.dbg.bytes_touched[row] : 0ull) + (uint64_t)n * sizeof(T);
+    }
+    if (a.dbg.topk_ids) {
+      const int32_t m = min(k, a.dbg.topk_stride);
+      for (int32_t j = lane; j < m; j += 32) {
+        a.dbg.topk_ids[(int64_t)row * a.dbg.topk_stride + j] = pos_to_id(a, (int64_t)fpos[j] + lo);
+        if (a.dbg.topk_ready) a.dbg.topk_ready[(int64_t)row * a.dbg.topk_stride + j] = fr[j];
+      }
+    }
+  }
+  sync();
+  lap(15);
+  return true;
+}
+
+}  // namespace dp

@@ -70,8 +70,8 @@ struct DrawResult {
   double margin;
 };
 
-DP_DEV DrawResult warp_filter_draw(const double* r, int32_t k, const dp_params_t& p, double u,
-                                   double* w, double* cum) {
+DP_DEV DrawResult warp_filter_draw_smem(const double* r, int32_t k, const dp_params_t& p, double u, double* w,
+                                        double* cum) {
   const uint32_t lane = lane_id();
   const double r0 = r[0];
   // w_j = exp(r_j - r_0) (filtering.py:90), inclusive cumsum in f64
@@ -89,8 +89,9 @@ DP_DEV DrawResult warp_filter_draw(const double* r, int32_t k, const dp_params_t
   __syncwarp();
   int32_t kept = k;
   double margin = 1e300;
+  const double total = cum[k - 1];
   if (p.top_p < 1.0) {                               // filtering.py:91-95
-    const double thr = p.top_p * cum[k - 1];
+    const double thr = p.top_p * total;
     int32_t below = 0;
     for (int32_t base = 0; base < k; base += 32) {
       const int32_t j = base + lane;
@@ -98,8 +99,8 @@ DP_DEV DrawResult warp_filter_draw(const double* r, int32_t k, const dp_params_t
     }
     const int32_t kp = below + 1;
     kept = min(kept, kp);
-    for (int32_t j = max(0, kp - 2); j < min(k, kp + 1); ++j)
-      margin = fmin(margin, fabs(cum[j] - thr) / cum[k - 1]);
+    for (int32_t j = max(0, kp - 2); j < min(k, kp + 1); ++j) margin = fmin(margin, fabs(cum[j] - thr));
+    margin /= total;
   }
   if (p.min_p > 0.0) {                               // filtering.py:96-98
     const double floor_ = p.min_p * w[0];
@@ -113,21 +114,80 @@ DP_DEV DrawResult warp_filter_draw(const double* r, int32_t k, const dp_params_t
   }
   kept = max(1, kept);                               // filtering.py:99
   const double S = cum[kept - 1];
+  const double us = u * S;
   // j* = #(cdf_j <= u), clamped (filtering.py:158-162)
   int32_t le = 0;
   for (int32_t base = 0; base < kept; base += 32) {
     const int32_t j = base + lane;
-    le += __popc(__ballot_sync(0xffffffffu, j < kept && cum[j] / S <= u));
+    le += __popc(__ballot_sync(0xffffffffu, j < kept && cum[j] <= us));
   }
   const int32_t js = min(le, kept - 1);
-  margin = fmin(margin, fabs(cum[js] / S - u));
-  if (js > 0) margin = fmin(margin, fabs(cum[js - 1] / S - u));
+  double dm = fabs(cum[js] - us);
+  if (js > 0) dm = fmin(dm, fabs(cum[js - 1] - us));
   DrawResult res;
   res.index = js;
   res.kept = kept;
   res.logprob = log(w[js] / S);
-  res.margin = margin;
+  res.margin = fmin(margin, dm / S);
   return res;
+}
+
+// k <= 64: everything in registers (two candidates per lane)
+DP_DEV DrawResult warp_filter_draw_reg(const double* r, int32_t k, const dp_params_t& p, double u) {
+  const uint32_t lane = lane_id();
+  const int32_t j0 = lane, j1 = lane + 32;
+  const double r0 = __shfl_sync(0xffffffffu, r[0], 0);
+  const double ra = j0 < k ? r[j0] : 0.0, rb = j1 < k ? r[j1] : 0.0;
+  const double wa = j0 < k ? exp(ra - r0) : 0.0;
+  const double wb = j1 < k ? exp(rb - r0) : 0.0;
+  const double ca = warp_incl_scan(wa);
+  const double tot_a = __shfl_sync(0xffffffffu, ca, 31);
+  const double cb = warp_incl_scan(wb) + tot_a;
+  const double total = __shfl_sync(0xffffffffu, cb, 31);
+  // value at global index j (any lane): cum / w via shuffles
+  auto cum_at = [&](int32_t j) -> double {
+    const double x = __shfl_sync(0xffffffffu, j < 32 ? ca : cb, j & 31);
+    return x;
+  };
+  auto w_at = [&](int32_t j) -> double { return __shfl_sync(0xffffffffu, j < 32 ? wa : wb, j & 31); };
+  int32_t kept = k;
+  double margin = 1e300;
+  if (p.top_p < 1.0) {
+    const double thr = p.top_p * total;
+    const int32_t below = __popc(__ballot_sync(0xffffffffu, j0 < k && ca < thr)) +
+                          __popc(__ballot_sync(0xffffffffu, j1 < k && cb < thr));
+    const int32_t kp = below + 1;
+    kept = min(kept, kp);
+    for (int32_t j = max(0, kp - 2); j < min(k, kp + 1); ++j) margin = fmin(margin, fabs(cum_at(j) - thr));
+    margin /= total;
+  }
+  if (p.min_p > 0.0) {
+    const double floor_ = p.min_p * 1.0;   // w_0 = exp(0) = 1
+    const int32_t ge = __popc(__ballot_sync(0xffffffffu, j0 < k && wa >= floor_)) +
+                       __popc(__ballot_sync(0xffffffffu, j1 < k && wb >= floor_));
+    kept = min(kept, ge);
+    for (int32_t j = max(0, ge - 1); j < min(k, ge + 1); ++j) margin = fmin(margin, fabs(w_at(j) - floor_));
+  }
+  kept = max(1, kept);
+  const double S = cum_at(kept - 1);
+  const double us = u * S;
+  const int32_t le = __popc(__ballot_sync(0xffffffffu, j0 < kept && ca <= us)) +
+                     __popc(__ballot_sync(0xffffffffu, j1 < kept && cb <= us));
+  const int32_t js = min(le, kept - 1);
+  double dm = fabs(cum_at(js) - us);
+  if (js > 0) dm = fmin(dm, fabs(cum_at(js - 1) - us));
+  DrawResult res;
+  res.index = js;
+  res.kept = kept;
+  res.logprob = log(w_at(js) / S);
+  res.margin = fmin(margin, dm / S);
+  return res;
+}
+
+DP_DEV DrawResult warp_filter_draw(const double* r, int32_t k, const dp_params_t& p, double u, double* w,
+                                   double* cum, int64_t* prof = nullptr) {
+  (void)prof;
+  return k <= 64 ? warp_filter_draw_reg(r, k, p, u) : warp_filter_draw_smem(r, k, p, u, w, cum);
 }
 
 }  // namespace dp

@@ -93,39 +93,45 @@ DP_DEV uint32_t warp_compact(uint64_t* buf, uint32_t cnt, uint64_t t) {
 }
 
 // Block-level threshold over an indexed source: get(i, &key) returns false for
-// empty slots, i in [0, n_slots).  hist: 256 u32 shared.  bcast: 4 u32 shared.
-// Every thread of the block must call it; returns the threshold to all.
-template <int NT, typename Get>
-DP_DEV uint64_t block_select_threshold(Get get, uint32_t n_slots, uint32_t cnt, uint32_t need,
-                                       uint32_t* hist, uint32_t* bcast) {
+// empty slots, i in [0, n_slots).  NT cooperating threads (index t) with
+// barrier `sync`; hist: 256 u32 shared; bcast: 4 u32 shared.  Returns the
+// threshold to all.
+template <int NT, typename Get, typename Sync>
+DP_DEV uint64_t group_select_threshold(Get get, uint32_t n_slots, uint32_t cnt, uint32_t need, uint32_t* hist,
+                                       uint32_t* bcast, uint32_t t, Sync sync) {
   if (cnt <= need || need == 0) return need == 0 ? ~0ull : 0ull;
-  const uint32_t tid = threadIdx.x;
   uint64_t prefix = 0, mask = 0;
   for (int shift = 56; shift >= 0; shift -= 8) {
-    for (uint32_t i = tid; i < 256; i += NT) hist[i] = 0u;
-    __syncthreads();
-    for (uint32_t i = tid; i < n_slots; i += NT) {
+    for (uint32_t i = t; i < 256; i += NT) hist[i] = 0u;
+    sync();
+    for (uint32_t i = t; i < n_slots; i += NT) {
       uint64_t k;
       if (get(i, k) && (k & mask) == prefix) atomicAdd(&hist[(uint32_t)(k >> shift) & 255u], 1u);
     }
-    __syncthreads();
-    if (tid < 32) {
+    sync();
+    if (t < 32) {
       const DigitHit h = warp_find_digit(hist, need);
-      if (tid == 0) {
+      if (t == 0) {
         bcast[0] = h.digit;
         bcast[1] = h.above;
         bcast[2] = h.inbin;
       }
     }
-    __syncthreads();
+    sync();
     const uint32_t d = bcast[0], above = bcast[1], inbin = bcast[2];
     prefix |= (uint64_t)d << shift;
     mask |= 255ull << shift;
     need -= above;
-    __syncthreads();
+    sync();
     if (inbin == need) break;
   }
   return prefix;
+}
+
+template <int NT, typename Get>
+DP_DEV uint64_t block_select_threshold(Get get, uint32_t n_slots, uint32_t cnt, uint32_t need, uint32_t* hist,
+                                       uint32_t* bcast) {
+  return group_select_threshold<NT>(get, n_slots, cnt, need, hist, bcast, threadIdx.x, [] { __syncthreads(); });
 }
 
 }  // namespace dp

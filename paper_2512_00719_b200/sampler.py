@@ -66,6 +66,7 @@ class Decisions:
     bytes_touched: "object" = None
     topk_ids: "object" = None
     topk_ready: "object" = None
+    stats: "object" = None   # int64[8] launch counters (see dp_debug_t.stats)
 
 
 class DecisionPlane:
@@ -132,6 +133,7 @@ class DecisionPlane:
                 d.margin = torch.empty(b, dtype=torch.float64, device=dev)
                 d.kept = torch.empty(b, dtype=torch.int32, device=dev)
                 d.bytes_touched = torch.zeros(b, dtype=torch.int64, device=dev)
+                d.stats = torch.zeros(24, dtype=torch.int64, device=dev)
                 if topk_stride:
                     d.topk_ids = torch.full((b, topk_stride), -1, dtype=torch.int32, device=dev)
                     d.topk_ready = torch.full((b, topk_stride), float("nan"), dtype=torch.float64, device=dev)
@@ -140,9 +142,9 @@ class DecisionPlane:
 
     def _debug_struct(self, d: Decisions, topk_stride: int, debug: bool) -> N.Debug:
         if not debug:
-            return N.Debug(None, None, 0, 0, None, None, d.alpha.data_ptr(), None)
+            return N.Debug(None, None, 0, 0, None, None, d.alpha.data_ptr(), None, None)
         return N.Debug(_ptr(d.topk_ids).value, _ptr(d.topk_ready).value, topk_stride, 0, d.margin.data_ptr(),
-                       d.kept.data_ptr(), d.alpha.data_ptr(), d.bytes_touched.data_ptr())
+                       d.kept.data_ptr(), d.alpha.data_ptr(), d.bytes_touched.data_ptr(), d.stats.data_ptr())
 
     # -- the hot path ----------------------------------------------------------
     def sample(self, logits, iteration: int, variant: str = VARIANT_FULL, uniforms=None, summary=None,

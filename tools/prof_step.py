@@ -1,0 +1,47 @@
+"""Minimal driver for ncu captures: build a workload and run a few steps.
+
+    python tools/prof_step.py --config c2 --variant full --steps 3
+"""
+
+import argparse
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+from paper_2512_00719_b200 import DecisionPlane, HotVocab, SamplingParams  # noqa: E402
+from paper_2512_00719_b200.synthetic import SyntheticSource  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--variant", default="full")
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--split", type=int, default=0)
+    ap.add_argument("--hot", type=int, default=16384)
+    ap.add_argument("--bf16", action="store_true")
+    args = ap.parse_args()
+    cfg = bench.CONFIGS[args.config]
+    v, b = cfg["V"], cfg["B"]
+    prompts = [np.random.default_rng(s).integers(0, v, 32) for s in range(b)]
+    src = SyntheticSource(v, device="cuda")
+    hot = HotVocab(v, src.hot_ordering()[: args.hot]) if args.variant == "shvs" else None
+    plane = DecisionPlane(v, [SamplingParams(**cfg["params"])] * b, prompts=prompts, hot=hot, split=args.split,
+                          max_generated=136)
+    perm = hot.device_maps(plane.device)[0] if hot is not None else None
+    dt = torch.bfloat16 if args.bf16 else torch.float32
+    x = src.generate(0, range(b), dtype=dt, perm=perm)
+    for i in range(args.steps):
+        plane.sample(x, i, variant=args.variant)
+    torch.cuda.synchronize()
+    print("done")
+
+
+if __name__ == "__main__":
+    main()
