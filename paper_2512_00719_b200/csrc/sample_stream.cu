@@ -314,7 +314,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_sample_kernel(Sample
     return MODE == kHot && ((bitmap[pos >> 5] >> (pos & 31)) & 1u);
   };
   auto accum = [&](float x, int64_t pos) {
-    if (MODE == kHot && !pen_bit(pos)) sh += (double)__expf(((x - mtau_hi) - mtau_lo) * inv_tau);
+    if (MODE == kHot && !pen_bit(pos)) sh += (double)expf(((x - mtau_hi) - mtau_lo) * inv_tau);
   };
 
   while (true) {

@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(NT, 3) topk_sample_kernel(SampleArgs a) {
   float thr_f = -INFINITY;
   double sh = 0.0;         // kHot: unpenalized hot mass of this thread's elements
   auto accum = [&](float x, int64_t pos) {
-    if (MODE == kHot && !pen_bit(pos)) sh += (double)__expf(((x - mtau_hi) - mtau_lo) * inv_tau);
+    if (MODE == kHot && !pen_bit(pos)) sh += (double)expf(((x - mtau_hi) - mtau_lo) * inv_tau);
   };
   // number of valid slots of an indexed candidate source (block-wide)
   auto count_valid = [&](auto get, uint32_t n_slots) -> uint32_t {

@@ -71,10 +71,10 @@ __global__ void __launch_bounds__(NT) row_summary_kernel(const T* logits, int64_
     if (!valid) return;
     if (plen > 0 && ((bitmap[pos >> 5] >> (pos & 31)) & 1u)) return;
     if (v > m) {
-      s = (m == -INFINITY) ? 0.0 : s * (double)__expf((m - v) * inv_tau);
+      s = (m == -INFINITY) ? 0.0 : s * (double)expf((m - v) * inv_tau);
       m = v;
     }
-    s += (double)__expf((v - m) * inv_tau);
+    s += (double)expf((v - m) * inv_tau);
   };
   const uintptr_t addr = reinterpret_cast<uintptr_t>(x);
   const int64_t a0 = min64(V, (int64_t)(((16u - (addr & 15u)) & 15u) / sizeof(T)));
@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(NT) hot_mass_curve_kernel(const T* logits, int
     for (int64_t pos = lo + threadIdx.x; pos < hi; pos += NT) {
       if (plen > 0 && ((bitmap[pos >> 5] >> (pos & 31)) & 1u)) continue;
       const float v = Elem<T>::get(x, pos);
-      s += (double)__expf(((v - c_hi) - c_lo) * inv_tau);
+      s += (double)expf(((v - c_hi) - c_lo) * inv_tau);
     }
     for (int32_t j = threadIdx.x; j < plen; j += NT) {
       const int64_t pos = inv_perm ? inv_perm[pids[j]] : pids[j];
