@@ -35,7 +35,10 @@ C1_PARAMS = dict(temperature=0.8, top_k=50, top_p=0.9, rep_penalty=1.1)
 CONFIGS = {
     "c1": dict(V=32000, B=64, dtype="f32", params=C1_PARAMS, name="llama2-32k-b64"),
     "c2": dict(V=152064, B=1024, dtype="f32", params=C2_PARAMS, name="qwen2.5-152k-b1024"),
-    "c4": dict(V=151936, B=8192, dtype="f32", params=C2_PARAMS, name="qwen3-151936-b8192"),
+    "c3": dict(V=128256, B=1024, dtype="f32", params=C2_PARAMS, name="llama3-128k-b1024-shvs-sweep"),
+    "c4": dict(V=151936, B=8192, dtype="f32", params=C2_PARAMS, name="qwen3-151936-b8192", strong=True),
+    "c5": dict(V=152064, B=16384, dtype="bf16", params=C2_PARAMS, name="qwen2.5-152k-b16384-bf16-mix",
+               mix=True),
 }
 METRIC = "sampled tokens/s at V=152k, B=1024; achieved HBM GB/s vs B200 peak"
 PROMPT_LEN = 32
@@ -178,6 +181,65 @@ def reference_arm(args, cfg):
 # ---------------------------------------------------------------------------
 # our arm
 
+def _graph(fn, k):
+    """Capture k calls of fn() (each given its step index) into one CUDA graph."""
+    import torch
+
+    g = torch.cuda.CUDAGraph()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        with torch.cuda.graph(g, stream=side):
+            for i in range(k):
+                fn(i)
+    torch.cuda.current_stream().wait_stream(side)
+    return g
+
+
+def _timed(g, dist=None, world=1):
+    """Device time of one replay (ms), barrier + synchronize on both sides, max over ranks."""
+    import torch
+
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0.record(st)
+    g.replay()
+    e1.record(st)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return ms
+
+
+MIX = [  # C5: heterogeneous per-row params (BASELINE configs[4])
+    dict(temperature=0.8, top_k=1),                                   # greedy
+    dict(temperature=0.8, top_k=50),                                  # top-k only
+    dict(temperature=0.8, top_p=0.9),                                 # top-p only
+    dict(temperature=0.8, min_p=0.05),                                # min-p
+    dict(C2_PARAMS),                                                  # penalties + k + p
+]
+PEN = dict(rep_penalty=1.1, presence_penalty=0.5, frequency_penalty=0.1)
+
+
+def row_params(cfg, b):
+    from paper_2512_00719_b200 import SamplingParams
+
+    if cfg.get("mix"):
+        kw = dict(MIX[b % len(MIX)])
+        if (b // len(MIX)) % 2 == 1:   # penalties on / off alternate
+            kw.update(PEN)
+        return SamplingParams(**kw, seed=0)
+    return SamplingParams(**cfg["params"], seed=0)
+
+
 def run_ours(args, cfg):
     import torch
     import torch.distributed as dist
@@ -193,131 +255,169 @@ def run_ours(args, cfg):
         build.build()
     if world > 1:
         dist.barrier()
-    from paper_2512_00719_b200 import DecisionPlane, SamplingParams
+    from paper_2512_00719_b200 import DecisionPlane, HotVocab, partition_batch
     from paper_2512_00719_b200.synthetic import SyntheticSource
 
-    v, b_local = cfg["V"], cfg["B"]
-    if args.config == "c4":  # strong scaling: the global batch is fixed
-        from paper_2512_00719_b200 import partition_batch
-
+    v = cfg["V"]
+    if cfg.get("strong"):   # C4: the global batch is fixed and split over the ranks
         lo, hi = partition_batch(cfg["B"], world)[rank]
-        b_local = hi - lo
-        row0 = lo
-        scaling = "strong"
+        b_local, row0, scaling = hi - lo, lo, "strong"
     else:
-        row0 = rank * b_local
-        scaling = "weak"
+        b_local, row0, scaling = cfg["B"], rank * cfg["B"], "weak"
     seq_ids = np.arange(row0, row0 + b_local, dtype=np.uint64)
     prompts = [np.random.default_rng(int(s)).integers(0, v, PROMPT_LEN) for s in seq_ids]
-    params = [SamplingParams(**cfg["params"], seed=0)] * b_local
-    plane = DecisionPlane(v, params, prompts=prompts, seq_ids=seq_ids, device=dev,
-                          max_generated=RESET_EVERY + 8, split=args.split)
+    params = [row_params(cfg, int(s)) for s in seq_ids]
     src = SyntheticSource(v, device=dev)
+    variant = args.variant if not cfg.get("mix") else "shvs"
+    hot = HotVocab(v, src.hot_ordering()[: args.hot]) if variant == "shvs" else None
+    plane = DecisionPlane(v, params, prompts=prompts, seq_ids=seq_ids, hot=hot, device=dev,
+                          max_generated=RESET_EVERY + 8, split=args.split)
     tdt = torch.float32 if cfg["dtype"] == "f32" else torch.bfloat16
-    bufs = [src.generate(i, seq_ids, dtype=tdt) for i in range(2)]   # 2 x 623 MB > L2
+    perm = hot.device_maps(dev)[0] if hot is not None else None
+    bufs = [src.generate(i, seq_ids, dtype=tdt, perm=perm) for i in range(2)]   # 2 x batch > L2
+    inv = hot.device_maps(dev)[1] if hot is not None else None
     gathered = torch.empty(b_local * world, dtype=torch.int32, device=dev)
-    st = torch.cuda.current_stream()
+    base_it = [0]
 
-    it = [0]
+    def sample_only(i):
+        it = base_it[0] + i
+        if variant == "shvs":
+            summ = plane.row_summary(bufs[it & 1], inv_perm=inv)
+            return plane.sample(bufs[it & 1], it, variant="shvs", summary=summ, update=False)
+        return plane.sample(bufs[it & 1], it, update=False)
 
-    def step(ev_pair=None):
-        i = it[0]
-        if i % RESET_EVERY == 0 and i > 0:
+    def step(i):
+        it = base_it[0] + i
+        if it % RESET_EVERY == 0 and it > 0:
             plane.state.reset()
-        if ev_pair is not None:
-            ev_pair[0].record(st)
-        d = plane.sample(bufs[i & 1], i, update=False)
-        if ev_pair is not None:
-            ev_pair[1].record(st)
+        d = sample_only(i)
         plane.state.update(d.token, d.flags)
         if world > 1:
             dist.all_gather_into_tensor(gathered, d.token)
-        it[0] += 1
         return d
 
-    for _ in range(args.warmup):
-        step()
+    for i in range(args.warmup):                     # eager warm-up (also JIT-free: kernels are prebuilt)
+        step(i)
+    base_it[0] = args.warmup
     torch.cuda.synchronize()
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    try:
+        g = _graph(step, args.steps)
+        graphed = True
+    except Exception as exc:   # e.g. a collective that cannot be captured
+        print(f"# graph capture failed ({exc}); timing eagerly", file=sys.stderr)
+        graphed = False
     with ClockSampler(local) as clk:
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        start.record(st)
-        for k in range(args.steps):
-            step(evs[k])
-        end.record(st)
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-    ms = start.elapsed_time(end)
-    kern_ms = [a.elapsed_time(b) for a, b in evs]
-    if world > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    total_tokens = b_local * world * args.steps if scaling == "weak" else cfg["B"] * args.steps
+        if graphed:
+            ms = _timed(g, dist, world)
+        else:
+            st = torch.cuda.current_stream()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            e0.record(st)
+            for i in range(args.steps):
+                step(i)
+            e1.record(st)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1)
+            if world > 1:
+                t = torch.tensor([ms], device=dev, dtype=torch.float64)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                ms = float(t.item())
+    total_tokens = (b_local * world if scaling == "weak" else cfg["B"]) * args.steps
     value = total_tokens / (ms / 1000.0)
 
-    # roofline of the dominant kernel (dp_sample_full): algorithmic bytes / launch
+    # dominant kernel(s): the sampling launch(es) alone, graph-replayed
+    kg = _graph(sample_only, args.kernel_steps)
+    torch.cuda.synchronize()
+    kern_ms = _timed(kg) / args.kernel_steps
+    d = sample_only(0)
+    torch.cuda.synchronize()
+    flags = d.flags.cpu().numpy()
+    accept = float(np.mean((flags & 0x02) != 0)) if variant == "shvs" else None
     pen_len = plane.state.len.float().mean().item()
     esz = 4 if cfg["dtype"] == "f32" else 2
-    bytes_per_row = v * esz + 8 * pen_len + 4 + 64 + 8 + 13
-    kern_avg_s = statistics.mean(kern_ms) / 1000.0
-    achieved = bytes_per_row * b_local / kern_avg_s / 1e9
+    small = 8 * pen_len + 4 + 64 + 8 + 13                # penalty list, params, seq id, outputs
+    if variant == "shvs":
+        # algorithmic bytes: producer summary pass (V) + hot prefix (H) + tail on rejection
+        h = args.hot
+        bytes_per_row = v * esz + h * esz + (1 - accept) * (v - h) * esz + 16 + small
+    else:
+        bytes_per_row = v * esz + small
+    achieved = bytes_per_row * b_local / (kern_ms / 1000.0) / 1e9
     peak, peak_kind = measured_peak()
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
-            traffic = json.load(fh).get(f"{args.config}_{args.variant}")
+            traffic = json.load(fh).get(f"{args.config}_{variant}")
     except Exception:
         pass
 
-    # e2e through the public API with host buffers (pinned), copies timed
-    e2e = None
-    if rank == 0 or world > 1:
-        host = bufs[0].cpu().pin_memory()
-        dbuf = torch.empty_like(bufs[0])
-        tok_host = torch.empty(b_local, dtype=torch.int32).pin_memory()
-        n_e2e = max(2, min(args.steps, 6))
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(st)
-        for k in range(n_e2e):
-            dbuf.copy_(host, non_blocking=True)
-            d = plane.sample(dbuf, 10_000 + k)
-            tok_host.copy_(d.token, non_blocking=True)
-        e1.record(st)
-        torch.cuda.synchronize()
-        e2e_s = e0.elapsed_time(e1) / 1000.0
-        e2e = {"value": b_local * world * n_e2e / e2e_s if scaling == "weak" else cfg["B"] * n_e2e / e2e_s,
-               "unit": "tokens/s", "h2d_bytes_per_step": int(host.numel() * host.element_size()),
-               "d2h_bytes_per_step": int(tok_host.numel() * 4), "steps": n_e2e}
+    # e2e through the public API with HOST buffers: pinned logits H2D, sample,
+    # token D2H, every step inside the timed region
+    st = torch.cuda.current_stream()
+    host = bufs[0].cpu().pin_memory()
+    dbuf = torch.empty_like(bufs[0])
+    tok_host = torch.empty(b_local, dtype=torch.int32).pin_memory()
+    n_e2e = max(2, min(args.steps, 6))
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for k in range(n_e2e):
+        dbuf.copy_(host, non_blocking=True)
+        if variant == "shvs":
+            dd = plane.sample(dbuf, 10_000 + k, variant="shvs", summary=plane.row_summary(dbuf, inv_perm=inv))
+        else:
+            dd = plane.sample(dbuf, 10_000 + k)
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, dd.token)
+            tok_host.copy_(gathered[rank * b_local:(rank + 1) * b_local], non_blocking=True)
+        else:
+            tok_host.copy_(dd.token, non_blocking=True)
+    e1.record(st)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e = {"value": (b_local * world if scaling == "weak" else cfg["B"]) * n_e2e / (e2e_ms / 1000.0),
+           "unit": "tokens/s", "h2d_bytes_per_step": int(host.numel() * host.element_size()),
+           "d2h_bytes_per_step": int(tok_host.numel() * 4), "steps": n_e2e,
+           "path": "DecisionPlane.sample on pinned host logits (H2D + sample + D2H per step)"}
 
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             x_rows = bufs[0][:64].float().cpu().numpy()
+            if hot is not None:   # back to token-id order for the reference law
+                x_rows = x_rows[:, hot.inv_perm]
             rate, cores, rows = cpu_baseline(x_rows, prompts[:64], cfg["params"], args.cpu_seconds)
             cpu = {"value": rate, "unit": "tokens/s", "cores": cores, "kind": "port",
                    "sample": f"64 rows of this workload looped for {args.cpu_seconds:.0f}s on {cores} processes "
-                             f"({rows} decisions), oracle port of _Sampler.sample+update_output_histogram"}
+                             f"({rows} decisions), oracle port of _Sampler.sample+update_output_histogram "
+                             "(full-vocabulary law)"}
+        launches = {"full": 2, "shvs": 6}[variant] + 1 + (1 if world > 1 else 0)
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic (SyntheticSource formula on device)",
-            "config": {"workload": cfg["name"], "V": v, "B_per_gpu": b_local, "variant": args.variant,
-                       "params": cfg["params"], "l2": "inputs larger than L2 (2 x batch buffers alternate)",
+            "config": {"workload": cfg["name"], "V": v, "B_per_gpu": b_local, "variant": variant,
+                       "hot_size": args.hot if variant == "shvs" else None,
+                       "params": "5-way mix" if cfg.get("mix") else cfg["params"],
+                       "l2": "inputs larger than L2 (2 x batch buffers alternate)",
+                       "timing": "CUDA graph of the K steps" if graphed else "eager",
                        "split": plane._plan.split},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                         "kernel": "dp_sample_full (topk_sample_kernel)", "kernel_ms": statistics.mean(kern_ms),
-                         "bytes_per_row": bytes_per_row},
+                         "kernel": "dp_sample_full" if variant == "full" else "dp_row_summary + dp_sample_shvs",
+                         "kernel_ms": kern_ms, "bytes_per_row": bytes_per_row},
+            "shvs_accept": accept,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": args.steps * (3 + (1 if world > 1 else 0)) + sum(
-                1 for i in range(args.warmup, args.warmup + args.steps) if i % RESET_EVERY == 0 and i > 0),
+            "gpu_launches": args.steps * launches + sum(
+                1 for i in range(args.warmup, args.warmup + args.steps) if i % RESET_EVERY == 0),
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -328,8 +428,10 @@ def run_ours(args, cfg):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--kernel-steps", type=int, default=50)
+    ap.add_argument("--hot", type=int, default=16384)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--variant", default="full", choices=["full", "shvs"])
