@@ -106,6 +106,8 @@ void plan_topk(dp::SampleArgs& a, const dp_plan_t* plan, int64_t B, int64_t n, i
   }
   if (split > 8) split = 8;
   a.split = split;
+  // threads per CTA: 256 by default; plan->reserved[0] may request 128
+  a.nt = (plan && plan->reserved[0] == 128) ? 128 : 256;
   (void)elem_bytes;
 }
 

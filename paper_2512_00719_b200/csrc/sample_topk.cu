@@ -82,7 +82,7 @@ __host__ __device__ inline TopkLayout topk_layout(int ccap, int kcap, int lcap, 
 
 
 template <typename T, int MODE, int NT, int U>
-__global__ void __launch_bounds__(NT, 3) topk_sample_kernel(SampleArgs a) {
+__global__ void __launch_bounds__(NT, 1024 / NT) topk_sample_kernel(SampleArgs a) {
   constexpr int NW = NT / 32;
   constexpr int EPV = Elem<T>::kPerVec;
   extern __shared__ __align__(16) uint8_t smem[];
@@ -408,9 +408,9 @@ __global__ void __launch_bounds__(NT, 3) topk_sample_kernel(SampleArgs a) {
 // ---------------------------------------------------------------------------
 // host launcher
 
-template <typename T, int MODE>
+template <typename T, int MODE, int NT>
 static cudaError_t launch_topk_t(const SampleArgs& a, int grid_rows, cudaStream_t st) {
-  constexpr int NT = 256, U = 8;
+  constexpr int U = 8;
   const int64_t n = MODE == kFull ? a.V : (MODE == kHot ? a.H : a.V - a.H);
   const int bm_words = MODE == kHot ? (int)((n + 31) / 32) : 0;
   const TopkLayout L = topk_layout<NT>(a.wcap, a.kcap, a.lcap, bm_words, a.split);
@@ -432,15 +432,21 @@ static cudaError_t launch_topk_t(const SampleArgs& a, int grid_rows, cudaStream_
   return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
-cudaError_t launch_topk(const SampleArgs& a, int dtype, int mode, int grid_rows, cudaStream_t st) {
+template <int NT>
+static cudaError_t launch_topk_nt(const SampleArgs& a, int dtype, int mode, int grid_rows, cudaStream_t st) {
   if (dtype == DP_F32) {
-    if (mode == kFull) return launch_topk_t<float, kFull>(a, grid_rows, st);
-    if (mode == kHot) return launch_topk_t<float, kHot>(a, grid_rows, st);
-    return launch_topk_t<float, kTail>(a, grid_rows, st);
+    if (mode == kFull) return launch_topk_t<float, kFull, NT>(a, grid_rows, st);
+    if (mode == kHot) return launch_topk_t<float, kHot, NT>(a, grid_rows, st);
+    return launch_topk_t<float, kTail, NT>(a, grid_rows, st);
   }
-  if (mode == kFull) return launch_topk_t<__nv_bfloat16, kFull>(a, grid_rows, st);
-  if (mode == kHot) return launch_topk_t<__nv_bfloat16, kHot>(a, grid_rows, st);
-  return launch_topk_t<__nv_bfloat16, kTail>(a, grid_rows, st);
+  if (mode == kFull) return launch_topk_t<__nv_bfloat16, kFull, NT>(a, grid_rows, st);
+  if (mode == kHot) return launch_topk_t<__nv_bfloat16, kHot, NT>(a, grid_rows, st);
+  return launch_topk_t<__nv_bfloat16, kTail, NT>(a, grid_rows, st);
+}
+
+cudaError_t launch_topk(const SampleArgs& a, int dtype, int mode, int grid_rows, cudaStream_t st) {
+  return a.nt == 128 ? launch_topk_nt<128>(a, dtype, mode, grid_rows, st)
+                     : launch_topk_nt<256>(a, dtype, mode, grid_rows, st);
 }
 
 }  // namespace dp

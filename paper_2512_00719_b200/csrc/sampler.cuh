@@ -31,6 +31,7 @@ struct SampleArgs {
   int32_t* reject_rows;         // kHot: rows appended on rejection
   int32_t* reject_count;
   int32_t wcap, kcap, lcap, split;
+  int32_t nt;                   // threads per CTA of the top-k kernel (128 / 256)
 };
 
 DP_DEV int64_t dom_lo(const SampleArgs& a, int mode) { return mode == kTail ? a.H : 0; }
