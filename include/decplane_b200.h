@@ -102,7 +102,10 @@ typedef struct {
 typedef struct {
   int32_t max_top_k;
   int32_t split;
-  int32_t reserved[6];
+  int32_t threads;      /* threads per CTA of the top-k kernel: 0/256 or 128 */
+  int32_t summary_raw;  /* dp_sample_shvs: row_max/total_expsum are the producer's raw
+                           summary (dp_row_summary_raw); correct it for penalties */
+  int32_t reserved[4];
 } dp_plan_t;
 
 /* Library / device info. dp_device_check returns DP_OK when `device` is sm_100. */
@@ -135,6 +138,16 @@ DP_API int dp_row_summary(const void* logits, int dtype, int64_t B, int64_t V, i
                    const dp_params_t* params, const dp_penalty_t* pen_host,
                    const int32_t* inv_perm, double* row_max, double* total_expsum,
                    void* stream);
+
+/* Producer-side raw summary: (max, sum exp) of x/tau per row WITHOUT
+ * penalties — what a logits producer (LM-head epilogue) can emit while writing
+ * the row.  dp_sample_shvs with plan->summary_raw = 1 corrects it exactly for
+ * the sparse penalty list (O(|list|) per row), so an SHVS step never streams
+ * the full row (the make_shard_blocks contract, service.py:470-504, paper
+ * section 5.3 "w can be pre-computed on GPUs when writing logits"). */
+DP_API int dp_row_summary_raw(const void* logits, int dtype, int64_t B, int64_t V, int64_t ld,
+                              const dp_params_t* params, double* row_max, double* total_expsum,
+                              void* stream);
 
 /* Speculative hot-vocab sampling on hot-first rows: split_decision
  * (shvs.py:198-255) as driven by _Sampler SHVS (service.py:354-380).  Touches

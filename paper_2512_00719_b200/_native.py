@@ -25,7 +25,7 @@ FLAG_DEGENERATE = 0x80
 EXPORTS = [
     "dp_version", "dp_device_check", "dp_last_error", "dp_uniforms", "dp_sample_full",
     "dp_row_summary", "dp_sample_shvs", "dp_penalty_update", "dp_penalty_reset",
-    "dp_ready_rows", "dp_synth_logits", "dp_hot_mass_curve",
+    "dp_ready_rows", "dp_synth_logits", "dp_hot_mass_curve", "dp_row_summary_raw",
 ]
 
 
@@ -65,7 +65,8 @@ class Debug(C.Structure):
 
 
 class Plan(C.Structure):
-    _fields_ = [("max_top_k", C.c_int32), ("split", C.c_int32), ("reserved", C.c_int32 * 6)]
+    _fields_ = [("max_top_k", C.c_int32), ("split", C.c_int32), ("threads", C.c_int32),
+                ("summary_raw", C.c_int32), ("reserved", C.c_int32 * 4)]
 
 
 assert C.sizeof(Params) == 64
@@ -79,6 +80,7 @@ _SIGS = {
     "dp_sample_full": ([_P, C.c_int, _I64, _I64, _I64, _P, C.POINTER(Penalty), _P, _P, _U64,
                         _P, _P, _P, C.POINTER(Debug), C.POINTER(Plan), _P], C.c_int),
     "dp_row_summary": ([_P, C.c_int, _I64, _I64, _I64, _P, C.POINTER(Penalty), _P, _P, _P, _P], C.c_int),
+    "dp_row_summary_raw": ([_P, C.c_int, _I64, _I64, _I64, _P, _P, _P, _P], C.c_int),
     "dp_sample_shvs": ([_P, C.c_int, _I64, _I64, _I64, _I64, _P, _P, _P, _P, _P, C.POINTER(Penalty),
                         _P, _P, _U64, _P, _P, _P, C.POINTER(Debug), C.POINTER(Plan), _P, _P], C.c_int),
     "dp_penalty_update": ([C.POINTER(Penalty), _P, _I64, _P, _P], C.c_int),

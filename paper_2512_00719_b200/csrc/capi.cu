@@ -107,7 +107,8 @@ void plan_topk(dp::SampleArgs& a, const dp_plan_t* plan, int64_t B, int64_t n, i
   if (split > 8) split = 8;
   a.split = split;
   // threads per CTA: 256 by default; plan->reserved[0] may request 128
-  a.nt = (plan && plan->reserved[0] == 128) ? 128 : 256;
+  a.nt = (plan && plan->threads == 128) ? 128 : 256;
+  a.summary_raw = (plan && plan->summary_raw) ? 1 : 0;
   (void)elem_bytes;
 }
 
@@ -185,6 +186,20 @@ int dp_row_summary(const void* logits, int dtype, int64_t B, int64_t V, int64_t 
   return cuda_status(dp::launch_row_summary(logits, dtype, B, V, ld, params, *pen_host, inv_perm, row_max,
                                             total_expsum, (cudaStream_t)stream),
                      "dp_row_summary");
+}
+
+int dp_row_summary_raw(const void* logits, int dtype, int64_t B, int64_t V, int64_t ld, const dp_params_t* params,
+                       double* row_max, double* total_expsum, void* stream) {
+  if (!logits || !params || !row_max || !total_expsum) return fail(DP_ERR_ARG, "dp_row_summary_raw: null argument%s");
+  if (dtype != DP_F32 && dtype != DP_BF16) return fail(DP_ERR_UNSUPPORTED, "dp_row_summary_raw: dtype%s");
+  if (B < 0 || V < 1 || ld < V) return fail(DP_ERR_ARG, "dp_row_summary_raw: bad shape%s");
+  if (B == 0) return DP_OK;
+  dp_penalty_t none;
+  std::memset(&none, 0, sizeof(none));
+  none.vocab_size = (int32_t)V;
+  return cuda_status(dp::launch_row_summary(logits, dtype, B, V, ld, params, none, nullptr, row_max, total_expsum,
+                                            (cudaStream_t)stream),
+                     "dp_row_summary_raw");
 }
 
 int dp_sample_shvs(const void* logits, int dtype, int64_t B, int64_t V, int64_t H, int64_t ld, const int32_t* perm,

@@ -31,6 +31,7 @@ struct FinishScratch {
   uint32_t nl;
   uint32_t pad;
   double sh_pen[32];
+  double corr[32];
 };
 
 // Penalty entries of a row whose loads are issued early (before the
@@ -182,6 +183,7 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
 
   // kHot: alpha and the accept test first (shvs.py:223-236)
   double alpha = 1.0;
+  bool imprecise = false;
   if (MODE == kHot) {
     double spen = 0.0;   // exact mass of penalized hot ids (f64)
     for (int32_t j = t; j < plen; j += NT) {
@@ -190,12 +192,26 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
       pen_entry(j, pos, x, c);
       if (pos >= 0) spen += exp(ready_penalized(x, c, p) - mrow);
     }
+    double scorr = 0.0;   // raw producer summary -> penalized total (shvs.py:148-154 needs the ready row)
+    if (a.summary_raw)
+      scorr = raw_summary_correction(a, row, p, plen, mrow, t, NT,
+                                     [&](int64_t pos) { return Elem<T>::get(rowp - lo, pos); });
     spen = warp_sum(spen);
-    if (lane == 0) fs.sh_pen[warp] = spen;
+    scorr = warp_sum(scorr);
+    if (lane == 0) {
+      fs.sh_pen[warp] = spen;
+      fs.corr[warp] = scorr;
+    }
     sync();
-    double sH = sh_unpen;
-    for (int w = 0; w < NT / 32; ++w) sH += fs.sh_pen[w];   // fixed order: deterministic
-    const double S = a.total_expsum[row];
+    double sH = sh_unpen, corr = 0.0;
+    for (int w = 0; w < NT / 32; ++w) {   // fixed order: deterministic
+      sH += fs.sh_pen[w];
+      corr += fs.corr[w];
+    }
+    const double S_prod = a.total_expsum[row];
+    const double S = S_prod + corr;
+    // a raw summary dominated by since-penalized mass loses relative precision
+    imprecise = a.summary_raw && S_prod > 16.0 * S;
     const bool tail_empty = a.V == a.H;
     bool degenerate = false;
     if (!tail_empty) {
@@ -207,7 +223,7 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
       if (t == 0) {
         uint8_t fl = DP_FLAG_REJECTED;
         if (degenerate || (tail_empty && !(sH > 0.0))) fl |= DP_FLAG_DEGENERATE;
-        else if (fabs(u[1] - alpha) < kBoundaryEps) fl |= DP_FLAG_NEAR_BOUNDARY;
+        else if (fabs(u[1] - alpha) < kBoundaryEps || imprecise) fl |= DP_FLAG_NEAR_BOUNDARY;
         a.flags[row] = fl;
         if (a.dbg.alpha) a.dbg.alpha[row] = alpha;
         if (a.dbg.margin) a.dbg.margin[row] = fabs(u[1] - alpha);
@@ -321,7 +337,7 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
       uint8_t fl = MODE == kHot ? DP_FLAG_ACCEPTED_HOT : (MODE == kTail ? DP_FLAG_REJECTED : 0);
       double margin = d.margin;
       if (MODE == kHot && a.V != a.H) margin = fmin(margin, fabs(u[1] - alpha));
-      if (margin < kBoundaryEps) fl |= DP_FLAG_NEAR_BOUNDARY;
+      if (margin < kBoundaryEps || imprecise) fl |= DP_FLAG_NEAR_BOUNDARY;
       if (MODE == kTail) fl |= a.flags[row] & DP_FLAG_NEAR_BOUNDARY;
       a.flags[row] = fl;
       if (a.dbg.margin) a.dbg.margin[row] = MODE == kTail ? fmin(margin, a.dbg.margin[row]) : margin;

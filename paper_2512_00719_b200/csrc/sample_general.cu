@@ -350,10 +350,19 @@ __global__ void __launch_bounds__(kGenNT, 1) general_sample_kernel(SampleArgs a)
   // kHot: alpha and the accept test (shvs.py:223-236); S_H relative to the
   // producer's row max m: S_H = W * exp(rmax - m)
   double alpha = 1.0;
+  bool imprecise = false;
   if (MODE == kHot) {
     const double mrow = a.row_max[row];
     const double sH = ((double)W / kFix) * exp(rmax - mrow);
-    const double S = a.total_expsum[row];
+    double corr = 0.0;
+    if (a.summary_raw) {
+      corr = raw_summary_correction(a, row, p, plen_all, mrow, tid, kGenNT,
+                                    [&](int64_t pos) { return Elem<T>::get(rowp - lo, pos); });
+      corr = blk_sum_d(corr, g, sync);
+    }
+    const double S_prod = a.total_expsum[row];
+    const double S = S_prod + corr;
+    imprecise = a.summary_raw && S_prod > 16.0 * S;
     const bool tail_empty = a.V == a.H;
     bool degenerate = false;
     if (!tail_empty) {
@@ -365,7 +374,7 @@ __global__ void __launch_bounds__(kGenNT, 1) general_sample_kernel(SampleArgs a)
       if (tid == 0) {
         uint8_t fl = DP_FLAG_REJECTED;
         if (degenerate || (tail_empty && !(sH > 0.0))) fl |= DP_FLAG_DEGENERATE;
-        else if (fabs(u[1] - alpha) < kBoundaryEps) fl |= DP_FLAG_NEAR_BOUNDARY;
+        else if (fabs(u[1] - alpha) < kBoundaryEps || imprecise) fl |= DP_FLAG_NEAR_BOUNDARY;
         a.flags[row] = fl;
         if (a.dbg.alpha) a.dbg.alpha[row] = alpha;
         if (a.dbg.margin) a.dbg.margin[row] = fabs(u[1] - alpha);
@@ -627,7 +636,7 @@ __global__ void __launch_bounds__(kGenNT, 1) general_sample_kernel(SampleArgs a)
     a.logprob[row] = (r - rmax) - log((double)S_kept / kFix);
     uint8_t fl = MODE == kHot ? DP_FLAG_ACCEPTED_HOT : (MODE == kTail ? DP_FLAG_REJECTED : 0);
     if (MODE == kHot && a.V != a.H) margin = fmin(margin, fabs(u[1] - alpha));
-    if (margin < kBoundaryEps) fl |= DP_FLAG_NEAR_BOUNDARY;
+    if (margin < kBoundaryEps || imprecise) fl |= DP_FLAG_NEAR_BOUNDARY;
     if (MODE == kTail) fl |= a.flags[row] & DP_FLAG_NEAR_BOUNDARY;
     a.flags[row] = fl;
     if (a.dbg.margin) a.dbg.margin[row] = MODE == kTail ? fmin(margin, a.dbg.margin[row]) : margin;

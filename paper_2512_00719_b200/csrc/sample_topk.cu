@@ -118,6 +118,15 @@ __global__ void __launch_bounds__(NT, 1024 / NT) topk_sample_kernel(SampleArgs a
   const uint32_t ccap = L.ccap;
 
   // ---- setup
+  const bool prof = a.dbg.stats != nullptr && threadIdx.x == 0;
+  long long pc0 = prof ? clock64() : 0;
+  auto lapk = [&](int slot) {
+    if (prof) {
+      const long long now = clock64();
+      atomicAdd((unsigned long long*)&a.dbg.stats[slot], (unsigned long long)(now - pc0));
+      pc0 = now;
+    }
+  };
   if (tid == 0) {
     ms.cnt = 0u;
     ms.overflow = 0u;
@@ -147,6 +156,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) topk_sample_kernel(SampleArgs a
   if (split > 1) cluster_sync();   // CTA 0's mbarrier is initialised before anyone arrives
   else __syncthreads();
 
+  lapk(17);
   // ---- segment geometry (32-bit vector indices: V < 2^31)
   const uintptr_t addr = reinterpret_cast<uintptr_t>(rowp);
   const int32_t a0 = (int32_t)min64(n, (int64_t)(((16u - (addr & 15u)) & 15u) / sizeof(T)));
@@ -341,6 +351,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) topk_sample_kernel(SampleArgs a
     __syncthreads();
   }
 
+  lapk(18);
   // ---- CTA-level exact top-kp
   {
     const uint32_t ns = min(ms.cnt, ccap) * EPV + (rank == 0 ? ms.nscal : 0u);
@@ -361,6 +372,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) topk_sample_kernel(SampleArgs a
   }
   const uint32_t nsel_own = ms.nsel;
 
+  lapk(19);
   // ---- push-model cluster merge into CTA 0 (DSMEM + mbarrier)
   if (split > 1) {
     if (rank != 0) {
@@ -397,6 +409,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) topk_sample_kernel(SampleArgs a
     __syncthreads();
   }
 
+  lapk(20);
   // ---- final stage (CTA 0): penalties, exact sort, filter, draw
   {
     const FinLayout F = fin_layout(a.lcap);

@@ -32,6 +32,7 @@ struct SampleArgs {
   int32_t* reject_count;
   int32_t wcap, kcap, lcap, split;
   int32_t nt;                   // threads per CTA of the top-k kernel (128 / 256)
+  int32_t summary_raw;          // kHot: row_max/total_expsum are the producer's raw summary
 };
 
 DP_DEV int64_t dom_lo(const SampleArgs& a, int mode) { return mode == kTail ? a.H : 0; }
@@ -56,6 +57,24 @@ DP_DEV void get_uniforms(const SampleArgs& a, int row, const dp_params_t& p, dou
 // number of penalty entries that can change values for this row
 DP_DEV int32_t pen_len(const SampleArgs& a, int row, const dp_params_t& p) {
   return penalties_neutral(p) ? 0 : a.pen.len[row];
+}
+
+// Total mass S of the ready row relative to `mrow` when the producer summary is
+// raw (no penalties): S = S_raw + sum over the penalty list of
+// [exp(r_j - m) - exp(x_j/tau - m)], exact f64 per entry.  Runs on NT threads
+// (index t), returns the per-thread partial of the correction; `x_at` reads a
+// raw logit at an absolute row position.  The caller reduces the partials.
+template <typename XAt>
+DP_DEV double raw_summary_correction(const SampleArgs& a, int row, const dp_params_t& p, int32_t plen, double mrow,
+                                     uint32_t t, uint32_t nt, XAt x_at) {
+  const int32_t* pids = a.pen.ids + (int64_t)row * a.pen.cap;
+  const int32_t* pcnt = a.pen.out_count + (int64_t)row * a.pen.cap;
+  double c = 0.0;
+  for (int32_t j = t; j < plen; j += nt) {
+    const float x = x_at(id_to_pos(a, pids[j]));
+    c += exp(ready_penalized(x, pcnt[j], p) - mrow) - exp(ready_plain(x, p) - mrow);
+  }
+  return c;
 }
 
 // ---------------------------------------------------------------------------

@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(NT) row_summary_kernel(const T* logits, int64_
   const int64_t row = blockIdx.x;
   const dp_params_t p = params[row];
   const T* x = logits + row * ld;
-  const int32_t plen = penalties_neutral(p) ? 0 : pen.len[row];
+  const int32_t plen = (penalties_neutral(p) || pen.len == nullptr) ? 0 : pen.len[row];
   const int32_t* pids = pen.ids + row * pen.cap;
   const int32_t* pcnt = pen.out_count + row * pen.cap;
   const uint32_t words = plen > 0 ? (uint32_t)((V + 31) / 32) : 0u;
@@ -189,7 +189,7 @@ cudaError_t launch_row_summary(const void* logits, int dtype, int64_t B, int64_t
                                const dp_params_t* params, const dp_penalty_t& pen, const int32_t* inv_perm,
                                double* row_max, double* total, cudaStream_t st) {
   constexpr int NT = 512, U = 4;
-  const size_t smem = 40 * 8 + 40 * 4 + (size_t)((V + 31) / 32) * 4;
+  const size_t smem = 40 * 8 + 40 * 4 + (pen.len ? (size_t)((V + 31) / 32) * 4 : 0);
   if (dtype == DP_F32) {
     auto k = row_summary_kernel<float, NT, U>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -148,12 +148,15 @@ class DecisionPlane:
 
     # -- the hot path ----------------------------------------------------------
     def sample(self, logits, iteration: int, variant: str = VARIANT_FULL, uniforms=None, summary=None,
-               update: bool = True, debug: bool = False, topk_stride: int = 0) -> Decisions:
+               update: bool = True, debug: bool = False, topk_stride: int = 0,
+               summary_raw: bool = False) -> Decisions:
         """One decision per row.  `logits` is a [B, V] CUDA tensor (fp32/bf16,
         unit stride along V) in vocab order for "full" and hot-first order for
         "shvs".  `summary` = (row_max, total_expsum) f64 tensors from the
         producer (make_shard_blocks contract, service.py:470-504); computed here
-        with one extra pass when omitted."""
+        with one extra pass when omitted.  With `summary_raw=True` the summary
+        is the producer's penalty-free one (`producer_summary`), corrected on
+        device for the sparse penalty list, so a step never re-reads the row."""
         if logits.dim() != 2 or logits.shape[0] != self.batch or logits.shape[1] != self.vocab_size:
             raise ValueError(f"logits must be [{self.batch}, {self.vocab_size}]")
         if not logits.is_cuda or logits.stride(1) != 1:
@@ -174,6 +177,7 @@ class DecisionPlane:
             if summary is None:
                 summary = self.row_summary(logits, inv_perm=inv)
             rmax, tot = summary
+            self._plan.summary_raw = 1 if summary_raw else 0
             N.call("dp_sample_shvs", _ptr(logits), dt, self.batch, self.vocab_size, self.hot.size,
                    logits.stride(0), _ptr(perm), _ptr(inv), _ptr(rmax), _ptr(tot), _ptr(self._params_dev),
                    C.byref(self.state.native), uni, _ptr(self._seq_dev), int(iteration), _ptr(d.token),
@@ -192,6 +196,17 @@ class DecisionPlane:
         tot = torch.empty(self.batch, dtype=torch.float64, device=self.device)
         N.call("dp_row_summary", _ptr(logits), _dtype_code(logits), self.batch, self.vocab_size, logits.stride(0),
                _ptr(self._params_dev), C.byref(self.state.native), _ptr(inv_perm), _ptr(rmax), _ptr(tot), _stream())
+        return rmax, tot
+
+    def producer_summary(self, logits):
+        """Penalty-free (row_max, total_expsum) of logits/tau: what a logits
+        producer emits while writing the rows (dp_row_summary_raw)."""
+        import torch
+
+        rmax = torch.empty(self.batch, dtype=torch.float64, device=self.device)
+        tot = torch.empty(self.batch, dtype=torch.float64, device=self.device)
+        N.call("dp_row_summary_raw", _ptr(logits), _dtype_code(logits), self.batch, self.vocab_size,
+               logits.stride(0), _ptr(self._params_dev), _ptr(rmax), _ptr(tot), _stream())
         return rmax, tot
 
     def uniforms(self, iteration: int):

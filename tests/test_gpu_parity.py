@@ -55,7 +55,7 @@ def compare(tag, gpu_tok, gpu_lp, dec, exempt_log):
     assert not bad, f"{tag}: token mismatches outside the boundary band: {bad[:8]}"
 
 
-def run_golden(torch, name, variant):
+def run_golden(torch, name, variant, raw_summary=False):
     case = Case(name)
     params = case.params()
     states = case.states()
@@ -71,7 +71,8 @@ def run_golden(torch, name, variant):
         xt = torch.from_numpy(x).cuda()
         if variant == "shvs":
             xt = plane.hot.to_hot_first(xt).contiguous()
-        d = plane.sample(xt, it, variant=variant, debug=True)
+        summ = plane.producer_summary(xt) if raw_summary else None
+        d = plane.sample(xt, it, variant=variant, debug=True, summary=summ, summary_raw=raw_summary)
         tok, lp = d.token.cpu().numpy(), d.logprob.cpu().numpy()
         compare(f"{name}/it{it}", tok, lp, dec, exempt)
         fl = d.flags.cpu().numpy()
@@ -130,6 +131,14 @@ def test_full_path_matches_reference_run(torch_cuda, name):
 @pytest.mark.parametrize("name", ["shvs_accept", "shvs_reject", "het_shvs", "shvs_neutral"])
 def test_shvs_matches_reference_run(torch_cuda, name):
     run_golden(torch_cuda, name, "shvs")
+
+
+@pytest.mark.parametrize("name", ["shvs_accept", "shvs_reject", "het_shvs"])
+def test_shvs_with_producer_raw_summary(torch_cuda, name):
+    """SHVS fed the producer's penalty-free summary, corrected on device for
+    the penalty list, must make the reference's decisions (which use the exact
+    penalized summary) — alpha agrees to ~1e-7."""
+    run_golden(torch_cuda, name, "shvs", raw_summary=True)
 
 
 def test_topk_sets_and_ready_values_exact(torch_cuda):
