@@ -271,7 +271,7 @@ def run_ours(args, cfg):
     variant = args.variant if not cfg.get("mix") else "shvs"
     hot = HotVocab(v, src.hot_ordering()[: args.hot]) if variant == "shvs" else None
     plane = DecisionPlane(v, params, prompts=prompts, seq_ids=seq_ids, hot=hot, device=dev,
-                          max_generated=RESET_EVERY + 8, split=args.split)
+                          max_generated=RESET_EVERY + 8, split=args.split, kernel=args.kernel)
     tdt = torch.float32 if cfg["dtype"] == "f32" else torch.bfloat16
     perm = hot.device_maps(dev)[0] if hot is not None else None
     bufs = [src.generate(i, seq_ids, dtype=tdt, perm=perm) for i in range(2)]   # 2 x batch > L2
@@ -418,7 +418,7 @@ def run_ours(args, cfg):
                        "params": "5-way mix" if cfg.get("mix") else cfg["params"],
                        "l2": "inputs larger than L2 (2 x batch buffers alternate)",
                        "timing": "CUDA graph of the K steps" if graphed else "eager",
-                       "split": plane._plan.split},
+                       "split": plane._plan.split, "kernel": plane._plan.kernel},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                          "kernel": "dp_sample_full" if variant == "full" else "dp_sample_shvs",
@@ -447,6 +447,7 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--variant", default="full", choices=["full", "shvs"])
     ap.add_argument("--split", type=int, default=0)
+    ap.add_argument("--kernel", type=int, default=0, help="dp_plan_t.kernel: 0 auto, 1 CTA/cluster, 2 warp-per-row")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-seconds", type=float, default=5.0)
     ap.add_argument("--ref-budget", type=float, default=90.0)

@@ -95,17 +95,25 @@ typedef struct {
 
 /* Launch plan supplied by the host (nullable -> conservative defaults).
  * max_top_k: upper bound of top_k over the rows of the call (0 = unknown);
- * rows whose top-k stage does not fit the planned capacity take the general
- * (radix) path, so the bound only affects speed, never results.
+ *   it sizes the top-k capacities.  Rows that do not fit take the general
+ *   (radix) path unless the bounds below promise there are none.
+ * min_top_k: lower bound of top_k over the rows (0 = some row may have top-k
+ *   off).  When BOTH bounds are nonzero they are promises about every row of
+ *   the call and kernels that no row can need are not launched; a row that
+ *   breaks the promise is left undecided.  0 / 0 is always safe.
  * split: CTAs per row cluster for the streaming kernels (0 = auto, <= 8;
- *        -1 = the persistent warp-specialised TMA-ring kernel). */
+ *   -1 = the persistent warp-specialised TMA-ring kernel).
+ * kernel: 0 = auto, 1 = per-row CTA / cluster kernel, 2 = warp-per-row kernel
+ *   for rows with top_k <= 64 (auto picks it for the SHVS hot pass at B >= SMs). */
 typedef struct {
   int32_t max_top_k;
   int32_t split;
   int32_t threads;      /* threads per CTA of the top-k kernel: 0/256 or 128 */
   int32_t summary_raw;  /* dp_sample_shvs: row_max/total_expsum are the producer's raw
                            summary (dp_row_summary_raw); correct it for penalties */
-  int32_t reserved[4];
+  int32_t min_top_k;
+  int32_t kernel;
+  int32_t reserved[2];
 } dp_plan_t;
 
 /* Library / device info. dp_device_check returns DP_OK when `device` is sm_100. */

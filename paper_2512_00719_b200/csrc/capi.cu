@@ -9,6 +9,7 @@
 namespace dp {
 cudaError_t launch_topk(const SampleArgs& a, int dtype, int mode, int grid_rows, cudaStream_t st);
 cudaError_t launch_general(const SampleArgs& a, int dtype, int mode, int grid_rows, cudaStream_t st);
+cudaError_t launch_warp(const SampleArgs& a, int dtype, int mode, int grid_rows, cudaStream_t st);
 cudaError_t launch_stream(const SampleArgs& a, int dtype, int mode, int grid, int32_t* work, cudaStream_t st);
 cudaError_t launch_row_summary(const void* logits, int dtype, int64_t B, int64_t V, int64_t ld,
                                const dp_params_t* params, const dp_penalty_t& pen, const int32_t* inv_perm,
@@ -76,6 +77,34 @@ cudaError_t launch_sampler(const dp::SampleArgs& a, int dtype, int mode, int64_t
   }
   return dp::launch_topk(a, dtype, mode, (int)B, st);
 }
+// Which kernels a call launches.  Every row is routed to exactly one kernel by
+// route_row (sampler.cuh); a kernel is skipped only when the plan's top-k
+// bounds (promises, see dp_plan_t) prove no row routes to it.
+struct Launches {
+  bool warp, topk, general;
+};
+Launches plan_launches(dp::SampleArgs& a, const dp_plan_t* plan, int mode, int64_t B, int64_t n, bool persistent) {
+  Launches L;
+  const int kernel = plan ? plan->kernel : 0;
+  const int64_t kmax = plan ? plan->max_top_k : 0, kmin = plan ? plan->min_top_k : 0;
+  const bool bounded = kmax > 0 && kmin > 0 && kmax < n;
+  const int64_t cap = a.pen.cap;
+  a.use_warp = 0;
+  if (!persistent && mode != dp::kTail && kernel != 1) {
+    const bool auto_warp = mode == dp::kHot && B >= sm_count() && n <= 65536;
+    a.use_warp = (kernel == 2 || auto_warp) ? 1 : 0;
+  }
+  // every row with top-k on fits the warp kernel / the top-k kernel
+  const bool all_warp = a.use_warp && bounded && kmax <= dp::kWarpKMax && cap <= dp::kWarpPenCap &&
+                        (kmax + cap <= dp::kWarpKpMax || n <= dp::kWarpKpMax);
+  const int64_t kp_topk = kmax + (mode == dp::kHot ? 0 : cap);
+  const bool all_topk = bounded && (kp_topk < n ? kp_topk : n) <= a.kcap && kmax + 2 * cap <= a.lcap;
+  L.warp = a.use_warp != 0;
+  L.topk = !all_warp;
+  L.general = !(all_warp || all_topk);
+  return L;
+}
+
 bool valid_pen(const dp_penalty_t* pen, int64_t V) {
   return pen && pen->ids && pen->out_count && pen->len && pen->cap >= 0 && pen->vocab_size == V;
 }
@@ -169,10 +198,15 @@ int dp_sample_full(const void* logits, int dtype, int64_t B, int64_t V, int64_t 
   plan_topk(a, plan_host, B, V, dtype == DP_F32 ? 4 : 2);
   const bool persistent = use_stream(B, plan_host);
   if (persistent) a.split = 1;
-  cudaError_t e = launch_sampler(a, dtype, dp::kFull, B, persistent, 0, st);
-  if (e != cudaSuccess) return cuda_status(e, "dp_sample_full/topk");
-  e = dp::launch_general(a, dtype, dp::kFull, (int)B, st);
-  return cuda_status(e, "dp_sample_full/general");
+  const Launches L = plan_launches(a, plan_host, dp::kFull, B, V, persistent);
+  cudaError_t e = cudaSuccess;
+  if (L.warp && (e = dp::launch_warp(a, dtype, dp::kFull, (int)B, st)) != cudaSuccess)
+    return cuda_status(e, "dp_sample_full/warp");
+  if (L.topk && (e = launch_sampler(a, dtype, dp::kFull, B, persistent, 0, st)) != cudaSuccess)
+    return cuda_status(e, "dp_sample_full/topk");
+  if (L.general && (e = dp::launch_general(a, dtype, dp::kFull, (int)B, st)) != cudaSuccess)
+    return cuda_status(e, "dp_sample_full/general");
+  return DP_OK;
 }
 
 int dp_row_summary(const void* logits, int dtype, int64_t B, int64_t V, int64_t ld, const dp_params_t* params,
@@ -248,10 +282,13 @@ int dp_sample_shvs(const void* logits, int dtype, int64_t B, int64_t V, int64_t 
   plan_topk(a, plan_host, B, H, dtype == DP_F32 ? 4 : 2);
   const bool persistent = use_stream(B, plan_host);
   if (persistent) a.split = 1;
-  e = launch_sampler(a, dtype, dp::kHot, B, persistent, 1, st);
-  if (e != cudaSuccess) return cuda_status(e, "dp_sample_shvs/hot-topk");
-  e = dp::launch_general(a, dtype, dp::kHot, (int)B, st);
-  if (e != cudaSuccess) return cuda_status(e, "dp_sample_shvs/hot-general");
+  const Launches L = plan_launches(a, plan_host, dp::kHot, B, H, persistent);
+  if (L.warp && (e = dp::launch_warp(a, dtype, dp::kHot, (int)B, st)) != cudaSuccess)
+    return cuda_status(e, "dp_sample_shvs/hot-warp");
+  if (L.topk && (e = launch_sampler(a, dtype, dp::kHot, B, persistent, 1, st)) != cudaSuccess)
+    return cuda_status(e, "dp_sample_shvs/hot-topk");
+  if (L.general && (e = dp::launch_general(a, dtype, dp::kHot, (int)B, st)) != cudaSuccess)
+    return cuda_status(e, "dp_sample_shvs/hot-general");
   if (H == V) return DP_OK;
   // tail pass over [H, V) for the rows the hot pass rejected
   dp::SampleArgs t = a;
@@ -261,10 +298,12 @@ int dp_sample_shvs(const void* logits, int dtype, int64_t B, int64_t V, int64_t 
   t.reject_count = nullptr;
   plan_topk(t, plan_host, B, V - H, dtype == DP_F32 ? 4 : 2);
   if (persistent) t.split = 1;
-  e = launch_sampler(t, dtype, dp::kTail, B, persistent, 2, st);
-  if (e != cudaSuccess) return cuda_status(e, "dp_sample_shvs/tail-topk");
-  e = dp::launch_general(t, dtype, dp::kTail, (int)B, st);
-  return cuda_status(e, "dp_sample_shvs/tail-general");
+  const Launches LT = plan_launches(t, plan_host, dp::kTail, B, V - H, persistent);
+  if (LT.topk && (e = launch_sampler(t, dtype, dp::kTail, B, persistent, 2, st)) != cudaSuccess)
+    return cuda_status(e, "dp_sample_shvs/tail-topk");
+  if (LT.general && (e = dp::launch_general(t, dtype, dp::kTail, (int)B, st)) != cudaSuccess)
+    return cuda_status(e, "dp_sample_shvs/tail-general");
+  return DP_OK;
 }
 
 int dp_penalty_update(const dp_penalty_t* pen_host, const int32_t* token, int64_t B, uint8_t* flags, void* stream) {

@@ -131,6 +131,14 @@ DP_DEV double ready_plain(float x, const dp_params_t& p) {
   return z;
 }
 
+// 2^x on the SFU (ex2.approx.ftz: relative error ~2^-22).  Used only for the
+// hot-mass accumulation, whose arguments are pre-centred on the row maximum.
+DP_DEV float ex2_fast(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // ---------------------------------------------------------------------------
 // warp helpers
 DP_DEV uint32_t lane_id() { return threadIdx.x & 31u; }

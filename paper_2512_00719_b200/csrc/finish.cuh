@@ -5,6 +5,7 @@
 #pragma once
 
 #include "sampler.cuh"
+#include "select.cuh"
 
 namespace dp {
 
@@ -14,8 +15,9 @@ struct FinLayout {
 };
 __host__ __device__ inline FinLayout fin_layout(int lcap) {
   FinLayout f;
-  f.hash_cap = 1;
+  f.hash_cap = 256;   // also the radix histogram of the top-k cut
   while (f.hash_cap < 2u * (uint32_t)lcap) f.hash_cap <<= 1;
+  if (lcap < 256) lcap = 256;   // the sorts pad the list to a power of two >= 128
   uint32_t o = 0;
   f.key = o; o += lcap * 8u;
   f.r = o; o += lcap * 8u;
@@ -110,6 +112,100 @@ DP_DEV void warp_reg_sort(uint64_t (&key)[E], uint32_t (&pos)[E]) {
       }
     }
   }
+}
+
+// The k largest of fkey[0,nl) (duplicates allowed) by (key desc, pos asc),
+// sorted into fkey/fpos[0, min(k,nl)).  One warp; arrays hold >= 256 entries
+// (>= nl).  For k <= 64 a radix cut first keeps every key >= the k-th largest
+// (ties at the cut included), so usually only 64 entries are sorted; nl <= 256
+// otherwise.  hist: 256 u32 scratch.
+template <int E>
+DP_DEV void warp_sort_regs(uint64_t* fkey, uint32_t* fpos);
+
+// k rounds of warp arg-max: only for lists of > 256 tied survivors
+DP_DEV void warp_select_sort_slow(uint64_t* fkey, uint32_t* fpos, uint32_t c, uint32_t k) {
+  const uint32_t lane = lane_id();
+  for (uint32_t i = 0; i < k && i < c; ++i) {
+    uint64_t bk = 0ull;
+    uint32_t bp = 0xFFFFFFFFu, bi = 0xFFFFFFFFu;
+    for (uint32_t j = i + lane; j < c; j += 32) {
+      const uint64_t kk = fkey[j];
+      const uint32_t pp = fpos[j];
+      if (bi == 0xFFFFFFFFu || kk > bk || (kk == bk && pp < bp)) { bk = kk; bp = pp; bi = j; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t ok = __shfl_xor_sync(0xffffffffu, bk, o);
+      const uint32_t op = __shfl_xor_sync(0xffffffffu, bp, o);
+      const uint32_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (oi != 0xFFFFFFFFu && (bi == 0xFFFFFFFFu || ok > bk || (ok == bk && op < bp))) { bk = ok; bp = op; bi = oi; }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      fkey[bi] = fkey[i];
+      fpos[bi] = fpos[i];
+      fkey[i] = bk;
+      fpos[i] = bp;
+    }
+    __syncwarp();
+  }
+}
+
+DP_DEV void warp_topk_sort(uint64_t* fkey, uint32_t* fpos, uint32_t nl, uint32_t k, uint32_t* hist) {
+  const uint32_t lane = lane_id();
+  uint32_t c = nl;
+  if (k <= 64 && nl > 64) {
+    uint64_t prefix = 0, mask = 0;
+    uint32_t need = k;
+    for (int shift = 56; shift >= 0; shift -= 8) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) hist[lane + 32 * i] = 0u;
+      __syncwarp();
+      for (uint32_t i = lane; i < nl; i += 32) {
+        const uint64_t kk = fkey[i];
+        if ((kk & mask) == prefix) atomicAdd(&hist[(uint32_t)(kk >> shift) & 255u], 1u);
+      }
+      __syncwarp();
+      const DigitHit h = warp_find_digit(hist, need);
+      prefix |= (uint64_t)h.digit << shift;
+      mask |= 255ull << shift;
+      need -= h.above;
+      __syncwarp();
+      if (h.inbin == need) break;
+    }
+    // keys >= prefix: the whole cut bucket, or (walk ran to the last digit)
+    // everything above plus all ties at the k-th value
+    uint32_t out = 0;
+    for (uint32_t base = 0; base < nl; base += 32) {
+      const uint32_t i = base + lane;
+      const uint64_t kk = i < nl ? fkey[i] : 0ull;
+      const uint32_t pp = i < nl ? fpos[i] : 0u;
+      const bool keep = i < nl && kk >= prefix;
+      const uint32_t m = __ballot_sync(0xffffffffu, keep);
+      __syncwarp();
+      if (keep) {
+        const uint32_t o = out + __popc(m & lanemask_lt());
+        fkey[o] = kk;
+        fpos[o] = pp;
+      }
+      out += __popc(m);
+      __syncwarp();
+    }
+    c = out;
+  }
+  if (c > 256) {
+    warp_select_sort_slow(fkey, fpos, c, k);
+    return;
+  }
+  const uint32_t cp = c <= 64 ? 64u : (c <= 128 ? 128u : 256u);
+  for (uint32_t i = c + lane; i < cp; i += 32) {
+    fkey[i] = 0ull;
+    fpos[i] = 0xFFFFFFFFu;
+  }
+  __syncwarp();
+  if (c <= 64) warp_sort_regs<2>(fkey, fpos);
+  else if (c <= 128) warp_sort_regs<4>(fkey, fpos);
+  else warp_sort_regs<8>(fkey, fpos);
 }
 
 template <int E>
@@ -241,16 +337,20 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
   }
 
   // penalized positions of this domain -> hash set (raw candidates defer to them)
+  // (kHot streamed around them already: no hash set needed)
   if (t == 0) fs.nl = 0u;
-  for (uint32_t i = t; i < hcap; i += NT) hash[i] = 0xFFFFFFFFu;
+  if (MODE != kHot)
+    for (uint32_t i = t; i < hcap; i += NT) hash[i] = 0xFFFFFFFFu;
   sync();
   for (int32_t j = t; j < plen; j += NT) {
     int32_t pos, c;
     float x;
     pen_entry(j, pos, x, c);
     if (pos >= 0) {
-      uint32_t h = ((uint32_t)pos * 2654435761u) & hmask;
-      while (atomicCAS(&hash[h], 0xFFFFFFFFu, (uint32_t)pos) != 0xFFFFFFFFu) h = (h + 1u) & hmask;
+      if (MODE != kHot) {
+        uint32_t h = ((uint32_t)pos * 2654435761u) & hmask;
+        while (atomicCAS(&hash[h], 0xFFFFFFFFu, (uint32_t)pos) != 0xFFFFFFFFu) h = (h + 1u) & hmask;
+      }
       const uint32_t s = atomicAdd(&fs.nl, 1u);
       fkey[s] = f64_key(ready_penalized(x, c, p));
       fpos[s] = (uint32_t)pos;
@@ -291,8 +391,7 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
   // for short lists, all NT threads in shared memory otherwise
   if (p2 <= 256) {
     if (warp == 0) {
-      if (p2 <= 128) warp_sort_regs<4>(fkey, fpos);
-      else warp_sort_regs<8>(fkey, fpos);
+      warp_topk_sort(fkey, fpos, nl, (uint32_t)k, hash);
       const uint32_t m = min((uint32_t)k, nl);
       for (uint32_t i = lane; i < m; i += 32) {
         const uint64_t kk = fkey[i];

@@ -187,13 +187,7 @@ __global__ void __launch_bounds__(kGenNT, 1) general_sample_kernel(SampleArgs a)
   const int row = a.rows ? a.rows[ridx] : ridx;
   const dp_params_t p = a.params[row];
   const int32_t plen_all = pen_len(a, row, p);
-  {
-    const int32_t k = p.top_k;
-    const uint32_t kp = (uint32_t)min64(n, (int64_t)k + (MODE == kHot ? 0 : plen_all));
-    const bool topk_row = k > 0 && (int64_t)k < n && kp <= (uint32_t)a.kcap &&
-                          (uint32_t)(k + 2 * plen_all) <= (uint32_t)a.lcap;
-    if (topk_row) return;                                   // streaming top-k kernel's row
-  }
+  if (route_row(a, MODE, p.top_k, plen_all, n) != kRouteGeneral) return;   // a streaming kernel's row
   const T* rowp = reinterpret_cast<const T*>(a.logits) + (int64_t)row * a.ld + lo;
   const int32_t* pids = a.pen.ids + (int64_t)row * a.pen.cap;
   const int32_t* pcnt = a.pen.out_count + (int64_t)row * a.pen.cap;

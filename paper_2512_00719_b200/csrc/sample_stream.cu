@@ -98,9 +98,7 @@ __host__ __device__ inline StreamLayout stream_layout(int ccap, int kcap, int lc
 // same routing rule as topk_sample_kernel / the general path
 template <int MODE>
 DP_DEV bool topk_route(const SampleArgs& a, const dp_params_t& p, int32_t plen, int64_t n) {
-  const int32_t k = p.top_k;
-  const uint32_t kp = (uint32_t)min64(n, (int64_t)k + (MODE == kHot ? 0 : plen));
-  return k > 0 && (int64_t)k < n && kp <= (uint32_t)a.kcap && (uint32_t)(k + 2 * plen) <= (uint32_t)a.lcap;
+  return route_row(a, MODE, p.top_k, plen, n) == kRouteTopk;
 }
 
 template <typename T, int MODE>

@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) topk_sample_kernel(SampleArgs a
   extern __shared__ __align__(16) uint8_t smem[];
   const int64_t n = dom_n(a, MODE);
   const int64_t lo = dom_lo(a, MODE);
-  const uint32_t bm_words = MODE == kHot ? (uint32_t)((n + 31) / 32) : 0u;
+  const uint32_t bm_words = MODE == kHot ? (uint32_t)((n + 31) / 32) + 1u : 0u;   // +1: vector window
   const TopkLayout L = topk_layout<NT>(a.wcap, a.kcap, a.lcap, (int)bm_words, a.split);
   uint64_t* cand = reinterpret_cast<uint64_t*>(smem + L.cand);
   uint64_t* recv = reinterpret_cast<uint64_t*>(smem + L.recv);
@@ -109,8 +109,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) topk_sample_kernel(SampleArgs a
   const int32_t k = p.top_k;
   // kHot excludes penalized ids from the stream (bitmap) so it needs no widening
   const uint32_t kp = (uint32_t)min64(n, (int64_t)k + (MODE == kHot ? 0 : plen));
-  if (!(k > 0 && (int64_t)k < n && kp <= (uint32_t)a.kcap && (uint32_t)(k + 2 * plen) <= (uint32_t)a.lcap))
-    return;                                                     // general-path row
+  if (route_row(a, MODE, k, plen, n) != kRouteTopk) return;     // another kernel's row
 
   const T* rowp = reinterpret_cast<const T*>(a.logits) + (int64_t)row * a.ld + lo;
   const int32_t* pids = a.pen.ids + (int64_t)row * a.pen.cap;
@@ -140,7 +139,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) topk_sample_kernel(SampleArgs a
   }
   double mrow = 0.0;
   float mtau_hi = 0.f, mtau_lo = 0.f;
-  const float inv_tau = (float)(1.0 / p.temperature);
+  const float s2 = (float)(1.4426950408889634 / p.temperature);
   if (MODE == kHot) {
     for (uint32_t i = tid; i < bm_words; i += NT) bitmap[i] = 0u;
     __syncthreads();
@@ -176,8 +175,25 @@ __global__ void __launch_bounds__(NT, 1024 / NT) topk_sample_kernel(SampleArgs a
   uint64_t thr = 0ull;     // admit keys >= thr
   float thr_f = -INFINITY;
   double sh = 0.0;         // kHot: unpenalized hot mass of this thread's elements
+  // hot mass: exp((x - m tau) / tau) = 2^(((x - hi) - lo) * log2e / tau); the
+  // argument is centred on the row maximum (hi/lo split keeps x - m tau
+  // exact near the top), pairwise f32 sums per vector, one f64 add per vector
+  auto hot_exp = [&](float x) -> float { return ex2_fast(((x - mtau_hi) - mtau_lo) * s2); };
   auto accum = [&](float x, int64_t pos) {
-    if (MODE == kHot && !pen_bit(pos)) sh += (double)expf(((x - mtau_hi) - mtau_lo) * inv_tau);
+    if (MODE == kHot && !pen_bit(pos)) sh += (double)hot_exp(x);
+  };
+  auto accum_vec = [&](const uint4& vv, int32_t idx) {
+    const uint32_t p0 = (uint32_t)(a0 + idx * EPV);
+    const uint32_t w = p0 >> 5;
+    const uint32_t pm = __funnelshift_r(bitmap[w], bitmap[w + 1], p0 & 31u);
+    float e[EPV];
+#pragma unroll
+    for (int i = 0; i < EPV; ++i) e[i] = ((pm >> i) & 1u) ? 0.f : hot_exp(vec_elem<T>(vv, i));
+#pragma unroll
+    for (int st = 1; st < EPV; st <<= 1)
+#pragma unroll
+      for (int i = 0; i < EPV; i += 2 * st) e[i] += e[i + st];
+    sh += (double)e[0];
   };
   // number of valid slots of an indexed candidate source (block-wide)
   auto count_valid = [&](auto get, uint32_t n_slots) -> uint32_t {
@@ -293,14 +309,20 @@ __global__ void __launch_bounds__(NT, 1024 / NT) topk_sample_kernel(SampleArgs a
 #pragma unroll
       for (int j = 0; j < U; ++j) {
         const int32_t idx = base + j * 32 + (int32_t)lane;
-        if (MODE == kHot && pass_no == 0 && idx < v_hi) {
-#pragma unroll
-          for (int e = 0; e < EPV; ++e) accum(vec_elem<T>(v[j], e), (int64_t)a0 + (int64_t)idx * EPV + e);
-        }
+        if (MODE == kHot && pass_no == 0 && idx < v_hi) accum_vec(v[j], idx);
         bool any = false;
 #pragma unroll
         for (int e = 0; e < EPV; ++e) any |= vec_elem<T>(v[j], e) >= thr_f;
-        if (any && idx < v_hi) vm |= 1u << j;
+        if (any && idx < v_hi) {
+          // exact (value, position) test: after an overflow cut the threshold
+          // is a full composite key, and ties at its value must not re-admit
+          // (guarantees every re-stream admits strictly fewer elements)
+          bool ex = false;
+#pragma unroll
+          for (int e = 0; e < EPV; ++e)
+            ex |= comp_key(vec_elem<T>(v[j], e), (uint32_t)(a0 + idx * EPV + e)) >= thr;
+          if (ex) vm |= 1u << j;
+        }
       }
       if (vm) {
         uint32_t slot = atomicAdd(&ms.cnt, (uint32_t)__popc(vm));
@@ -425,7 +447,7 @@ template <typename T, int MODE, int NT>
 static cudaError_t launch_topk_t(const SampleArgs& a, int grid_rows, cudaStream_t st) {
   constexpr int U = 8;
   const int64_t n = MODE == kFull ? a.V : (MODE == kHot ? a.H : a.V - a.H);
-  const int bm_words = MODE == kHot ? (int)((n + 31) / 32) : 0;
+  const int bm_words = MODE == kHot ? (int)((n + 31) / 32) + 1 : 0;
   const TopkLayout L = topk_layout<NT>(a.wcap, a.kcap, a.lcap, bm_words, a.split);
   auto kern = topk_sample_kernel<T, MODE, NT, U>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);

@@ -33,6 +33,7 @@ struct SampleArgs {
   int32_t wcap, kcap, lcap, split;
   int32_t nt;                   // threads per CTA of the top-k kernel (128 / 256)
   int32_t summary_raw;          // kHot: row_max/total_expsum are the producer's raw summary
+  int32_t use_warp;             // this call runs the warp-per-row kernel (sample_warp.cu)
 };
 
 DP_DEV int64_t dom_lo(const SampleArgs& a, int mode) { return mode == kTail ? a.H : 0; }
@@ -57,6 +58,28 @@ DP_DEV void get_uniforms(const SampleArgs& a, int row, const dp_params_t& p, dou
 // number of penalty entries that can change values for this row
 DP_DEV int32_t pen_len(const SampleArgs& a, int row, const dp_params_t& p) {
   return penalties_neutral(p) ? 0 : a.pen.len[row];
+}
+
+// ---------------------------------------------------------------------------
+// Row routing: every row of a call is decided by exactly one kernel.
+//  * warp-per-row kernel (short top-k, sample_warp.cu) when the call uses it;
+//  * per-row CTA / cluster streaming top-k kernel (sample_topk.cu);
+//  * general radix kernel (no top-k / oversized lists, sample_general.cu).
+enum Route : int { kRouteGeneral = 0, kRouteTopk = 1, kRouteWarp = 2 };
+constexpr int kWarpKMax = 64;     // top_k limit of the warp kernel
+constexpr int kWarpKpMax = 256;   // raw candidates kept (k + penalty list)
+constexpr int kWarpPenCap = 256;  // penalty-list capacity it can hash
+
+DP_DEV bool warp_row_ok(const SampleArgs& a, int32_t k, int32_t plen, int64_t n) {
+  return k > 0 && (int64_t)k < n && k <= kWarpKMax && min64(n, (int64_t)k + plen) <= kWarpKpMax &&
+         a.pen.cap <= kWarpPenCap;
+}
+DP_DEV int route_row(const SampleArgs& a, int mode, int32_t k, int32_t plen, int64_t n) {
+  if (a.use_warp && warp_row_ok(a, k, plen, n)) return kRouteWarp;
+  const uint32_t kp = (uint32_t)min64(n, (int64_t)k + (mode == kHot ? 0 : plen));
+  if (k > 0 && (int64_t)k < n && kp <= (uint32_t)a.kcap && (uint32_t)(k + 2 * plen) <= (uint32_t)a.lcap)
+    return kRouteTopk;
+  return kRouteGeneral;
 }
 
 // Total mass S of the ready row relative to `mrow` when the producer summary is

@@ -73,7 +73,8 @@ class DecisionPlane:
     """A batch of B sequences with per-row params and GPU penalty state."""
 
     def __init__(self, vocab_size: int, params, prompts=None, seq_ids=None, hot: HotVocab | None = None,
-                 device="cuda", max_generated: int = 256, pen_cap: int | None = None, split: int = 0):
+                 device="cuda", max_generated: int = 256, pen_cap: int | None = None, split: int = 0,
+                 kernel: int = 0):
         import torch
 
         self.device = torch.device(device)
@@ -92,6 +93,7 @@ class DecisionPlane:
         self.state = PenaltyState(prompts, vocab_size, cap=pen_cap, device=self.device, max_generated=max_generated)
         self.hot = hot
         self.split = int(split)
+        self.kernel = int(kernel)   # dp_plan_t.kernel: 0 auto, 1 CTA/cluster, 2 warp-per-row
         self.set_params(params)
         self._out = None
         self._scratch = torch.empty(self.batch + 1, dtype=torch.int32, device=self.device)
@@ -110,7 +112,11 @@ class DecisionPlane:
         raw = np.frombuffer(params_bytes(self.params), dtype=np.uint8).copy()
         self._params_dev = torch.from_numpy(raw).to(self.device)
         ks = [p.top_k for p in self.params if p.top_k > 0]
+        # exact bounds over the rows: they let the library skip kernels no row needs
+        min_k = min(p.top_k for p in self.params) if self.params else 0
         self._plan = N.Plan(max(ks) if ks else 0, self.split)
+        self._plan.min_top_k = max(0, min_k) if ks else 0
+        self._plan.kernel = self.kernel
 
     def set_hot(self, hot: HotVocab | None) -> None:
         """Hot-set changes land between iterations (service.py:602-610, :646-648)."""

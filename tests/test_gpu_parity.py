@@ -32,13 +32,17 @@ def torch_cuda():
     return torch
 
 
-def plane_for(torch, vocab, params, prompts, hot_ids=None, max_generated=64, split=0):
+def plane_for(torch, vocab, params, prompts, hot_ids=None, max_generated=64, split=0, kernel=0):
     from paper_2512_00719_b200 import DecisionPlane, HotVocab, SamplingParams
 
     hot = HotVocab(vocab, hot_ids) if hot_ids is not None else None
     sp = [SamplingParams(**vars(p)) for p in params]
     return DecisionPlane(vocab, sp, prompts=prompts, hot=hot, device="cuda", max_generated=max_generated,
-                         split=split)
+                         split=split, kernel=kernel)
+
+
+# dp_plan_t.kernel: 1 = per-row CTA / cluster kernel, 2 = warp-per-row kernel
+KERNELS = [1, 2]
 
 
 def compare(tag, gpu_tok, gpu_lp, dec, exempt_log):
@@ -55,12 +59,12 @@ def compare(tag, gpu_tok, gpu_lp, dec, exempt_log):
     assert not bad, f"{tag}: token mismatches outside the boundary band: {bad[:8]}"
 
 
-def run_golden(torch, name, variant, raw_summary=False):
+def run_golden(torch, name, variant, raw_summary=False, kernel=0):
     case = Case(name)
     params = case.params()
     states = case.states()
     plane = plane_for(torch, case.vocab, params, [case.prompts[b] for b in range(case.batch)],
-                      hot_ids=case.hot_ids)
+                      hot_ids=case.hot_ids, kernel=kernel)
     exempt = []
     for it in range(case.iters):
         x = case.logits(it)
@@ -123,32 +127,36 @@ def test_synthetic_logits_match_oracle_generator(torch_cuda):
     np.testing.assert_allclose(x, ref, rtol=2e-7, atol=0)
 
 
+@pytest.mark.parametrize("kernel", KERNELS)
 @pytest.mark.parametrize("name", ["c1_full", "c2_full", "het_full"])
-def test_full_path_matches_reference_run(torch_cuda, name):
-    run_golden(torch_cuda, name, "full")
+def test_full_path_matches_reference_run(torch_cuda, name, kernel):
+    run_golden(torch_cuda, name, "full", kernel=kernel)
 
 
+@pytest.mark.parametrize("kernel", KERNELS)
 @pytest.mark.parametrize("name", ["shvs_accept", "shvs_reject", "het_shvs", "shvs_neutral"])
-def test_shvs_matches_reference_run(torch_cuda, name):
-    run_golden(torch_cuda, name, "shvs")
+def test_shvs_matches_reference_run(torch_cuda, name, kernel):
+    run_golden(torch_cuda, name, "shvs", kernel=kernel)
 
 
+@pytest.mark.parametrize("kernel", KERNELS)
 @pytest.mark.parametrize("name", ["shvs_accept", "shvs_reject", "het_shvs"])
-def test_shvs_with_producer_raw_summary(torch_cuda, name):
+def test_shvs_with_producer_raw_summary(torch_cuda, name, kernel):
     """SHVS fed the producer's penalty-free summary, corrected on device for
     the penalty list, must make the reference's decisions (which use the exact
     penalized summary) — alpha agrees to ~1e-7."""
-    run_golden(torch_cuda, name, "shvs", raw_summary=True)
+    run_golden(torch_cuda, name, "shvs", raw_summary=True, kernel=kernel)
 
 
-def test_topk_sets_and_ready_values_exact(torch_cuda):
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_topk_sets_and_ready_values_exact(torch_cuda, kernel):
     torch = torch_cuda
     v, bsz, k = 32000, 64, 50
     params = [O.Params(temperature=0.8, top_k=k, top_p=0.9, rep_penalty=1.1, presence_penalty=0.3,
                        frequency_penalty=0.05, seed=b) for b in range(bsz)]
     prompts = [np.random.default_rng(b).integers(0, v, 32) for b in range(bsz)]
     states = [O.State.new(p, v) for p in prompts]
-    plane = plane_for(torch, v, params, prompts)
+    plane = plane_for(torch, v, params, prompts, kernel=kernel)
     src = O.Synthetic(v)
     for it in range(3):
         x = src.wire(it, range(bsz))
@@ -189,7 +197,8 @@ def test_penalized_ready_rows_bit_exact(torch_cuda):
         np.testing.assert_array_equal(got[b], O.ready_row(x[b], states[b], params[b]))
 
 
-def test_full_size_c2_properties_and_sampled_parity(torch_cuda):
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_full_size_c2_properties_and_sampled_parity(torch_cuda, kernel):
     """C2 at full size (V=152064, B=1024): every row through the GPU; a row
     sample through the oracle; size-independent properties on all rows."""
     torch = torch_cuda
@@ -201,7 +210,7 @@ def test_full_size_c2_properties_and_sampled_parity(torch_cuda):
     params = [O.Params(**kw, seed=0) for _ in range(bsz)]
     prompts = [np.random.default_rng(b).integers(0, v, 32) for b in range(bsz)]
     states = [O.State.new(p, v) for p in prompts]
-    plane = plane_for(torch, v, params, prompts, max_generated=16)
+    plane = plane_for(torch, v, params, prompts, max_generated=16, kernel=kernel)
     src = SyntheticSource(v, device="cuda")
     check_rows = list(range(0, bsz, 37))
     exempt = []
@@ -222,4 +231,65 @@ def test_full_size_c2_properties_and_sampled_parity(torch_cuda):
         compare(f"c2full/it{it}", tok[check_rows], lp[check_rows], dec, exempt)
         for b in range(bsz):
             states[b].update(int(tok[b]))
+    print("exemptions:", exempt)
+
+
+def adversarial_rows(v, bsz, seed=5):
+    """Rows that stress threshold estimation, buffer cuts and tie rules."""
+    rs = np.random.default_rng(seed)
+    x = np.empty((bsz, v), np.float32)
+    for b in range(bsz):
+        kind = b % 8
+        if kind == 0:
+            x[b] = 1.0                                            # all tied
+        elif kind == 1:
+            x[b] = np.arange(v, dtype=np.float32) * 1e-3            # ascending ramp
+        elif kind == 2:
+            x[b] = -np.arange(v, dtype=np.float32) * 1e-3           # descending ramp
+        elif kind == 3:
+            x[b] = rs.normal(size=v).astype(np.float32)
+            lo = rs.integers(0, v - 600)
+            x[b, lo:lo + 600] += 8.0                              # one dense spike cluster
+        elif kind == 4:
+            x[b] = np.round(rs.normal(size=v) * 4) / 4             # coarse values: many ties
+        elif kind == 5:
+            x[b] = -30.0
+            x[b, rs.integers(0, v, 3)] = 5.0                       # fewer spikes than k
+        elif kind == 6:
+            x[b] = rs.normal(size=v).astype(np.float32)
+            x[b, : v // 2] = -np.inf                              # -inf half
+        else:
+            import torch
+            x[b] = torch.from_numpy(rs.normal(size=v).astype(np.float32) * 3).bfloat16().float().numpy()
+    return x
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_adversarial_rows_match_oracle(torch_cuda, kernel):
+    torch = torch_cuda
+    v, bsz = 8192, 32
+    params = [O.Params(temperature=[0.7, 1.0, 1.5][b % 3], top_k=[50, 1, 64, 20][b % 4],
+                       top_p=[0.9, 1.0, 0.5][b % 3], min_p=[0.0, 0.05][b % 2],
+                       rep_penalty=[1.0, 1.3][b % 2], presence_penalty=[0.0, 0.4][(b // 2) % 2], seed=b)
+              for b in range(bsz)]
+    prompts = [np.random.default_rng(100 + b).integers(0, v, 48) for b in range(bsz)]
+    states = [O.State.new(p, v) for p in prompts]
+    plane = plane_for(torch, v, params, prompts, kernel=kernel)
+    exempt = []
+    for it in range(3):
+        x = adversarial_rows(v, bsz, seed=it)
+        d = plane.sample(torch.from_numpy(x).cuda(), it, debug=True, topk_stride=64)
+        tok, lp = d.token.cpu().numpy(), d.logprob.cpu().numpy()
+        ids = d.topk_ids.cpu().numpy()
+        dec = [O.sample_full_row(x[b], states[b], params[b], O.uniforms_per_row([params[b].seed], it, [b])[0])
+               for b in range(bsz)]
+        compare(f"adv/k{kernel}/it{it}", tok, lp, dec, exempt)
+        for b in range(bsz):
+            r = O.ready_row(x[b], states[b], params[b])
+            want = O.top_k_ids(r, params[b].top_k)
+            order = np.lexsort((want, -r[want]))
+            np.testing.assert_array_equal(ids[b, : params[b].top_k], want[order], err_msg=f"row {b}")
+        for b in range(bsz):
+            states[b].update(int(dec[b].token))
+        plane.state.update(torch.from_numpy(np.array([dd.token for dd in dec], np.int32)).cuda())
     print("exemptions:", exempt)
