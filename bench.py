@@ -105,19 +105,64 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # CPU reference arm (oracle port of the reference algorithm, on host cores)
 
-def _cpu_worker(args):
-    x, prompts, params, it0, seconds = args
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def reference_available() -> bool:
+    """The unmodified reference package installed by pip --target baseline/_ref."""
+    return os.path.isdir(os.path.join(REF_DIR, "decplane"))
+
+
+def _ref_worker(args):
+    """The reference's own sampler loop (harness.py:255-279): per iteration the
+    producer make_shard_blocks (service.py:470-504, untimed like the harness),
+    then per row _Sampler("offload-truncate").sample + update_output_histogram
+    (timed).  Returns (rows decided, seconds inside the timed calls)."""
+    x, prompts, params, seq0, seconds = args
+    sys.path.insert(0, REF_DIR)
+    from decplane import rng as ref_rng
+    from decplane.core import SamplingParams as RP, new_sequence_state
+    from decplane.penalty import update_output_histogram as ref_update
+    from decplane.service import EngineConfig, _Sampler, make_shard_blocks
+    from decplane.shvs import HotVocab as RHot
+    from decplane.transport import assemble_view
+
+    n, v = x.shape
+    cfg = EngineConfig(vocab_size=v, batch_size=n)
+    states = [new_sequence_state(seq0 + b, list(prompts[b]), v) for b in range(n)]
+    p = RP(**params)
+    sampler = _Sampler("offload-truncate", RHot(v, np.arange(v)))
+    col_major = np.ascontiguousarray(x.T).astype(np.float64)     # (V, B) wire layout, core.py:186-199
+    rows, busy, it, t_start = 0, 0.0, 0, time.perf_counter()
+    while True:
+        blocks = make_shard_blocks(cfg, it, col_major, states, lambda b: p)
+        view = assemble_view(blocks, (0, n))
+        for b in range(n):
+            draws = ref_rng.pregenerate_slice(p.seed, it, [seq0 + b])[0]
+            t0 = time.perf_counter()
+            d = sampler.sample(view, b, seq0 + b, states[b], p, draws, it)
+            ref_update(states[b], d.token_id)
+            busy += time.perf_counter() - t0
+            rows += 1
+        it += 1
+        if time.perf_counter() - t_start >= seconds:
+            break
+    return rows, busy
+
+
+def _port_worker(args):
+    """Fallback when baseline/_ref is absent: the oracle port of the same law."""
+    x, prompts, params, seq0, seconds = args
     from oracle import decplane_oracle as O
 
     v = x.shape[1]
     states = [O.State.new(p, v) for p in prompts]
     pp = O.Params(**params)
     t0 = time.perf_counter()
-    n = 0
-    it = it0
+    n, it = 0, 0
     while True:
         for b in range(x.shape[0]):
-            u = O.pregenerate_slice(pp.seed, it, [b])[0]
+            u = O.pregenerate_slice(pp.seed, it, [seq0 + b])[0]
             d = O.sample_full_row(x[b], states[b], pp, u)
             states[b].update(d.token)
             n += 1
@@ -128,19 +173,36 @@ def _cpu_worker(args):
 
 
 def cpu_baseline(x_rows: np.ndarray, prompts, params, seconds: float, cores: int | None = None):
-    """The reference decision law (oracle port) timed on this host's cores: one
-    process per core, rows split by partition_batch (transport.py:133-144)."""
+    """The reference CPU sampler timed on this host's cores: one process per
+    core (the reference's m-sampler design, service.py:584-589, without the
+    GIL), rows split by partition_batch (transport.py:133-144).  Uses the
+    unmodified reference from baseline/_ref when installed ("reference"), else
+    the oracle port ("port").  Returns (tokens/s, processes, rows, kind)."""
     import multiprocessing as mp
 
     cores = cores or len(os.sched_getaffinity(0))
-    parts = np.array_split(np.arange(x_rows.shape[0]), cores)
-    jobs = [(x_rows[p], [prompts[i] for i in p], params, 0, seconds) for p in parts if len(p)]
+    kind = "reference" if reference_available() else "port"
+    worker = _ref_worker if kind == "reference" else _port_worker
+    idx = np.arange(x_rows.shape[0])
+    parts = [idx[lo:hi] for lo, hi in _partition(x_rows.shape[0], min(cores, x_rows.shape[0]))]
+    jobs = [(x_rows[p], [prompts[i] for i in p], params, int(p[0]), seconds) for p in parts if len(p)]
     ctx = mp.get_context("fork")
     with ctx.Pool(len(jobs)) as pool:
-        res = pool.map(_cpu_worker, jobs)
+        res = pool.map(worker, jobs)
     rows = sum(r[0] for r in res)
-    wall = max(r[1] for r in res)
-    return rows / wall, len(jobs), rows
+    # every process decides its rows concurrently: aggregate rate = sum of per-process rates
+    rate = sum(r[0] / r[1] for r in res if r[1] > 0)
+    return rate, len(jobs), rows, kind
+
+
+def _partition(n, m):
+    base, rem = divmod(n, m)
+    out, lo = [], 0
+    for j in range(m):
+        hi = lo + base + (j < rem)
+        out.append((lo, hi))
+        lo = hi
+    return out
 
 
 def reference_arm(args, cfg):
@@ -150,7 +212,7 @@ def reference_arm(args, cfg):
     from oracle import decplane_oracle as O
 
     v = cfg["V"]
-    nrows = 64
+    nrows = int(min(cfg["B"], max(64, len(os.sched_getaffinity(0)))))
     src = O.Synthetic(v)
     x = src.wire(0, range(nrows))
     prompts = [np.random.default_rng(b).integers(0, v, PROMPT_LEN) for b in range(nrows)]
@@ -161,19 +223,21 @@ def reference_arm(args, cfg):
         cpu_baseline(x, prompts, cfg["params"], per_step)
     total_rows, total_t = 0, 0.0
     for _ in range(args.steps):
-        rate, cores, rows = cpu_baseline(x, prompts, cfg["params"], per_step)
+        rate, cores, rows, kind = cpu_baseline(x, prompts, cfg["params"], per_step)
         steps.append(rate)
         total_rows += rows
         total_t += rows / rate
     value = total_rows / total_t
+    what = ("unmodified reference (baseline/_ref) _Sampler('offload-truncate').sample + "
+            "update_output_histogram, producer make_shard_blocks untimed as in harness.py:255-279"
+            if kind == "reference" else "oracle port of _Sampler.sample + update_output_histogram")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * cfg["B"] / value,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (SyntheticSource formula, seed 0)",
             "config": {"workload": cfg["name"], "V": v, "B": cfg["B"], "params": cfg["params"]},
-            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port",
-                             "sample": f"{nrows} rows of the workload, {per_step:.2f}s per step, "
-                                       "oracle port of _Sampler.sample+update_output_histogram"},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": kind,
+                             "sample": f"{nrows} rows of the workload, {per_step:.2f}s per step, {what}"},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -181,8 +245,9 @@ def reference_arm(args, cfg):
 # ---------------------------------------------------------------------------
 # our arm
 
-def _graph(fn, k):
-    """Capture k calls of fn() (each given its step index) into one CUDA graph."""
+def _graph(fn, k, join=None):
+    """Capture k calls of fn() (each given its step index) into one CUDA graph;
+    join() re-joins any side stream the steps forked before capture ends."""
     import torch
 
     g = torch.cuda.CUDAGraph()
@@ -192,6 +257,8 @@ def _graph(fn, k):
         with torch.cuda.graph(g, stream=side):
             for i in range(k):
                 fn(i)
+            if join is not None:
+                join()
     torch.cuda.current_stream().wait_stream(side)
     return g
 
@@ -255,16 +322,17 @@ def run_ours(args, cfg):
         build.build()
     if world > 1:
         dist.barrier()
-    from paper_2512_00719_b200 import DecisionPlane, HotVocab, partition_batch
+    from paper_2512_00719_b200 import DecisionPlane, HotVocab
+    from paper_2512_00719_b200.sharded import BatchShard
     from paper_2512_00719_b200.synthetic import SyntheticSource
 
     v = cfg["V"]
-    if cfg.get("strong"):   # C4: the global batch is fixed and split over the ranks
-        lo, hi = partition_batch(cfg["B"], world)[rank]
-        b_local, row0, scaling = hi - lo, lo, "strong"
-    else:
-        b_local, row0, scaling = cfg["B"], rank * cfg["B"], "weak"
-    seq_ids = np.arange(row0, row0 + b_local, dtype=np.uint64)
+    # C4: the global batch is fixed and split over the ranks (strong); the
+    # other configs keep B rows per GPU (weak).  Rows: partition_batch blocks.
+    scaling = "strong" if cfg.get("strong") else "weak"
+    shard = BatchShard(cfg["B"] if scaling == "strong" else cfg["B"] * world, world, rank)
+    b_local = shard.rows
+    seq_ids = shard.seq_ids
     prompts = [np.random.default_rng(int(s)).integers(0, v, PROMPT_LEN) for s in seq_ids]
     params = [row_params(cfg, int(s)) for s in seq_ids]
     src = SyntheticSource(v, device=dev)
@@ -276,7 +344,9 @@ def run_ours(args, cfg):
     perm = hot.device_maps(dev)[0] if hot is not None else None
     bufs = [src.generate(i, seq_ids, dtype=tdt, perm=perm) for i in range(2)]   # 2 x batch > L2
     inv = hot.device_maps(dev)[1] if hot is not None else None
-    gathered = torch.empty(b_local * world, dtype=torch.int32, device=dev)
+    gathered = torch.empty(shard.batch_size, dtype=torch.int32, device=dev)
+    tok_pp = [torch.empty(b_local, dtype=torch.int32, device=dev) for _ in range(2)]
+    gstream = torch.cuda.Stream(device=dev)
     base_it = [0]
     # SHVS: the producer emits a penalty-free row summary with the logits
     # (LM-head epilogue); the sampler corrects it for the penalty list, so a
@@ -298,15 +368,26 @@ def run_ours(args, cfg):
         d = sample_only(i)
         plane.state.update(d.token, d.flags)
         if world > 1:
-            dist.all_gather_into_tensor(gathered, d.token)
+            # token-id all-gather on a side stream: it overlaps the next step's
+            # sampling (the penalty update needs only the local tokens)
+            cur = torch.cuda.current_stream()
+            tok_pp[it & 1].copy_(d.token)
+            gstream.wait_stream(cur)
+            with torch.cuda.stream(gstream):
+                shard.gather(tok_pp[it & 1], out=gathered)
         return d
+
+    def join():
+        if world > 1:
+            torch.cuda.current_stream().wait_stream(gstream)
 
     for i in range(args.warmup):                     # eager warm-up (also JIT-free: kernels are prebuilt)
         step(i)
+    join()
     base_it[0] = args.warmup
     torch.cuda.synchronize()
     try:
-        g = _graph(step, args.steps)
+        g = _graph(step, args.steps, join)
         graphed = True
     except Exception as exc:   # e.g. a collective that cannot be captured
         print(f"# graph capture failed ({exc}); timing eagerly", file=sys.stderr)
@@ -323,6 +404,7 @@ def run_ours(args, cfg):
             e0.record(st)
             for i in range(args.steps):
                 step(i)
+            join()
             e1.record(st)
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1)
@@ -330,7 +412,7 @@ def run_ours(args, cfg):
                 t = torch.tensor([ms], device=dev, dtype=torch.float64)
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
                 ms = float(t.item())
-    total_tokens = (b_local * world if scaling == "weak" else cfg["B"]) * args.steps
+    total_tokens = shard.batch_size * args.steps
     value = total_tokens / (ms / 1000.0)
 
     # dominant kernel(s): the sampling launch(es) alone, graph-replayed
@@ -381,8 +463,8 @@ def run_ours(args, cfg):
         else:
             dd = plane.sample(dbuf, 10_000 + k)
         if world > 1:
-            dist.all_gather_into_tensor(gathered, dd.token)
-            tok_host.copy_(gathered[rank * b_local:(rank + 1) * b_local], non_blocking=True)
+            shard.gather(dd.token, out=gathered)
+            tok_host.copy_(gathered[shard.lo:shard.hi], non_blocking=True)
         else:
             tok_host.copy_(dd.token, non_blocking=True)
     e1.record(st)
@@ -392,7 +474,7 @@ def run_ours(args, cfg):
         t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
-    e2e = {"value": (b_local * world if scaling == "weak" else cfg["B"]) * n_e2e / (e2e_ms / 1000.0),
+    e2e = {"value": shard.batch_size * n_e2e / (e2e_ms / 1000.0),
            "unit": "tokens/s", "h2d_bytes_per_step": int(host.numel() * host.element_size()),
            "d2h_bytes_per_step": int(tok_host.numel() * 4), "steps": n_e2e,
            "path": "DecisionPlane.sample on pinned host logits (H2D + sample + D2H per step)"}
@@ -400,14 +482,17 @@ def run_ours(args, cfg):
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            x_rows = bufs[0][:64].float().cpu().numpy()
+            nrows = int(min(b_local, max(64, len(os.sched_getaffinity(0)))))
+            x_rows = bufs[0][:nrows].float().cpu().numpy()
             if hot is not None:   # back to token-id order for the reference law
                 x_rows = x_rows[:, hot.inv_perm]
-            rate, cores, rows = cpu_baseline(x_rows, prompts[:64], cfg["params"], args.cpu_seconds)
-            cpu = {"value": rate, "unit": "tokens/s", "cores": cores, "kind": "port",
-                   "sample": f"64 rows of this workload looped for {args.cpu_seconds:.0f}s on {cores} processes "
-                             f"({rows} decisions), oracle port of _Sampler.sample+update_output_histogram "
-                             "(full-vocabulary law)"}
+            rate, cores, rows, kind = cpu_baseline(x_rows, prompts[:nrows], cfg["params"], args.cpu_seconds)
+            what = ("unmodified reference (baseline/_ref) _Sampler('offload-truncate').sample + "
+                    "update_output_histogram" if kind == "reference" else
+                    "oracle port of _Sampler.sample + update_output_histogram")
+            cpu = {"value": rate, "unit": "tokens/s", "cores": cores, "kind": kind,
+                   "sample": f"{nrows} rows of this workload (full-vocabulary law, same logits) looped for "
+                             f"{args.cpu_seconds:.0f}s on {cores} processes ({rows} decisions), {what}"}
         launches = {"full": 2, "shvs": 5}[variant] + 1 + (1 if world > 1 else 0)
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
