@@ -31,18 +31,22 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
+    """Compile + link the library.  `defines` / `out` build an A-B variant
+    (e.g. defines=["DP_MW_BLOCKS=6"], out=".../_lib/variants/x.so")."""
+    lib = out or LIB
+    if not force and not defines and out is None and not _stale():
         return LIB
     from concurrent.futures import ThreadPoolExecutor
 
     os.makedirs(LIBDIR, exist_ok=True)
-    objdir = os.path.join(ROOT, "build", "obj")
+    objdir = os.path.join(ROOT, "build", "obj" if not defines else "obj_" + "_".join(defines).replace("=", ""))
     os.makedirs(objdir, exist_ok=True)
     common = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
               "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
     if verbose:
         common += ["-Xptxas", "-v"]
+    common += ["-D" + d for d in defines]
 
     def compile_one(src):
         obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")
@@ -57,14 +61,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
             raise RuntimeError(f"nvcc failed compiling {src}")
         if verbose:
             sys.stderr.write(r.stderr)
-    link = [NVCC, *ARCH, "--shared", "-o", LIB + ".tmp"] + [obj for _, obj, _ in results]
+    os.makedirs(os.path.dirname(lib), exist_ok=True)
+    link = [NVCC, *ARCH, "--shared", "-o", lib + ".tmp"] + [obj for _, obj, _ in results]
     r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc failed linking libdecplane_b200.so")
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    outs = [a[6:] for a in sys.argv[1:] if a.startswith("--out=")]
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, defines=defs, out=outs[0] if outs else None))

@@ -12,7 +12,7 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libdecplane_b200.so")
+LIB_PATH = os.environ.get("DP_LIB") or os.path.join(_HERE, "_lib", "libdecplane_b200.so")   # DP_LIB: tools / A-B variants
 
 DP_OK, DP_ERR_ARG, DP_ERR_CUDA, DP_ERR_UNSUPPORTED, DP_ERR_CAPACITY = 0, -1, -2, -3, -4
 DP_F32, DP_BF16 = 0, 1

@@ -297,9 +297,19 @@ int dp_sample_shvs(const void* logits, int dtype, int64_t B, int64_t V, int64_t 
   t.reject_rows = nullptr;
   t.reject_count = nullptr;
   plan_topk(t, plan_host, B, V - H, dtype == DP_F32 ? 4 : 2);
+  // The tail pass serves only the rejected rows (typically a few percent of
+  // B, count known on the device only): 8-CTA clusters split each row over 8
+  // SMs, and the clusters loop over the reject list, so a handful of
+  // rejections costs one short row time rather than one long one.
+  int64_t tail_clusters = B;
+  if (!persistent && !(plan_host && plan_host->split > 0)) {
+    t.split = (V - H) >= 8 * 4096 ? 8 : 1;
+    const int64_t slots = (int64_t)sm_count() * 2 / t.split;   // resident clusters (2 tail CTAs per SM)
+    tail_clusters = B < slots ? B : slots;
+  }
   if (persistent) t.split = 1;
   const Launches LT = plan_launches(t, plan_host, dp::kTail, B, V - H, persistent);
-  if (LT.topk && (e = launch_sampler(t, dtype, dp::kTail, B, persistent, 2, st)) != cudaSuccess)
+  if (LT.topk && (e = launch_sampler(t, dtype, dp::kTail, tail_clusters, persistent, 2, st)) != cudaSuccess)
     return cuda_status(e, "dp_sample_shvs/tail-topk");
   if (LT.general && (e = dp::launch_general(t, dtype, dp::kTail, (int)B, st)) != cudaSuccess)
     return cuda_status(e, "dp_sample_shvs/tail-general");

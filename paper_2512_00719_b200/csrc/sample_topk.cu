@@ -82,7 +82,7 @@ __host__ __device__ inline TopkLayout topk_layout(int ccap, int kcap, int lcap, 
 
 
 template <typename T, int MODE, int NT, int U>
-__global__ void __launch_bounds__(NT, 1024 / NT) topk_sample_kernel(SampleArgs a) {
+__global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample_kernel(SampleArgs a) {
   constexpr int NW = NT / 32;
   constexpr int EPV = Elem<T>::kPerVec;
   extern __shared__ __align__(16) uint8_t smem[];
@@ -100,16 +100,22 @@ __global__ void __launch_bounds__(NT, 1024 / NT) topk_sample_kernel(SampleArgs a
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u;
   const uint32_t split = (uint32_t)a.split;
   const uint32_t rank = split > 1 ? cluster_ctarank() : 0u;
-  const int ridx = blockIdx.x / split;
   const int nrows = a.row_count ? *a.row_count : a.n_rows;
-  if (ridx >= nrows) return;                                    // uniform per cluster
+  // clusters loop over rows (the tail pass launches fewer clusters than rows);
+  // CTA 0's mbarrier completes one phase per row
+  if (split > 1 && rank == 0 && tid == 0) {
+    mbar_init(&ms.mbar, split - 1);
+    fence_mbar_init();
+  }
+  uint32_t phase = 0;
+  for (int ridx = blockIdx.x / (int)split; ridx < nrows; ridx += gridDim.x / split) {
   const int row = a.rows ? a.rows[ridx] : ridx;
   const dp_params_t p = a.params[row];
   const int32_t plen = pen_len(a, row, p);
   const int32_t k = p.top_k;
   // kHot excludes penalized ids from the stream (bitmap) so it needs no widening
   const uint32_t kp = (uint32_t)min64(n, (int64_t)k + (MODE == kHot ? 0 : plen));
-  if (route_row(a, MODE, k, plen, n) != kRouteTopk) return;     // another kernel's row
+  if (route_row(a, MODE, k, plen, n) != kRouteTopk) continue;   // another kernel's row (cluster-uniform)
 
   const T* rowp = reinterpret_cast<const T*>(a.logits) + (int64_t)row * a.ld + lo;
   const int32_t* pids = a.pen.ids + (int64_t)row * a.pen.cap;
@@ -132,10 +138,6 @@ __global__ void __launch_bounds__(NT, 1024 / NT) topk_sample_kernel(SampleArgs a
     ms.nsel = 0u;
     ms.nl = 0u;
     ms.nscal = 0u;
-    if (split > 1 && rank == 0) {
-      mbar_init(&ms.mbar, split - 1);
-      fence_mbar_init();
-    }
   }
   double mrow = 0.0;
   float mtau_hi = 0.f, mtau_lo = 0.f;
@@ -406,9 +408,11 @@ __global__ void __launch_bounds__(NT, 1024 / NT) topk_sample_kernel(SampleArgs a
       }
       __syncthreads();
       if (tid == 0) mbar_remote_arrive(dsmem_addr(&ms.mbar, 0));
-      return;
+      cluster_sync();   // end of row: CTA 0 is done with the receive buffers
+      phase ^= 1u;
+      continue;
     }
-    if (warp == 0) mbar_wait_parity(&ms.mbar, 0);   // one warp polls; the rest park on the barrier
+    if (warp == 0) mbar_wait_parity(&ms.mbar, phase);   // one warp polls; the rest park on the barrier
     __syncthreads();
     // gather own + received survivors into the merge scratch, exact select
     uint64_t* mrg = cand;
@@ -437,6 +441,13 @@ __global__ void __launch_bounds__(NT, 1024 / NT) topk_sample_kernel(SampleArgs a
     const FinLayout F = fin_layout(a.lcap);
     finish_row<T, MODE, NT>(a, row, p, plen, rowp, lo, n, sel, ms.nsel, sh_cta, mrow, smem + L.cand, F, ms.fin, tid,
                             [] { __syncthreads(); });
+  }
+  if (split > 1) {
+    cluster_sync();   // end of row: the receive buffers may be rewritten
+    phase ^= 1u;
+  } else {
+    __syncthreads();
+  }
   }
 }
 

@@ -75,6 +75,33 @@ DP_DEV uint64_t warp_select_threshold(const uint64_t* buf, uint32_t cnt, uint32_
   return prefix;
 }
 
+// Warp-level: the r-th largest (1-based) of n u32 keys (duplicates allowed),
+// or a value t below it with exactly r keys >= t (the walk stops once a whole
+// digit bucket is taken).  Either way at least r keys are >= the result.
+DP_DEV uint32_t warp_kth_u32(const uint32_t* keys, uint32_t n, uint32_t r, uint32_t* hist) {
+  if (r == 0u) return 0xFFFFFFFFu;
+  if (r > n) return 0u;
+  const uint32_t lane = lane_id();
+  uint32_t prefix = 0u, mask = 0u, need = r;
+  for (int shift = 24; shift >= 0; shift -= 8) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) hist[lane + 32 * i] = 0u;
+    __syncwarp();
+    for (uint32_t i = lane; i < n; i += 32) {
+      const uint32_t k = keys[i];
+      if ((k & mask) == prefix) atomicAdd(&hist[(k >> shift) & 255u], 1u);
+    }
+    __syncwarp();
+    const DigitHit h = warp_find_digit(hist, need);
+    prefix |= h.digit << shift;
+    mask |= 255u << shift;
+    need -= h.above;
+    __syncwarp();
+    if (h.inbin == need) break;
+  }
+  return prefix;
+}
+
 // In-place stable compaction of buf[0,cnt) keeping keys >= t; returns new count.
 DP_DEV uint32_t warp_compact(uint64_t* buf, uint32_t cnt, uint64_t t) {
   const uint32_t lane = lane_id();

@@ -1,3 +1,4 @@
-cd "${GRAFT_REPO_ROOT:-/root/repo}"
-timeout 900 python -m pytest tests -m gpu -x -q -rs --durations=8 > gpurun_out/pytest_r2c.txt 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_r2c.txt
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launch_shvs_r2c.csv python tools/prof_step.py --variant shvs --steps 3 > /dev/null 2>&1
+cd "${GRAFT_REPO_ROOT:-/root/repo}"; O=gpurun_out/it15; mkdir -p $O
+timeout 900 python -m pytest tests -m gpu -x -q > $O/pytest.txt 2>&1; echo "rc=$?" >> $O/pytest.txt
+DP_LIB=paper_2512_00719_b200/_lib/variants/prof.so python tools/phase_prof.py --variant shvs > $O/phase.txt 2>&1
+timeout 300 python bench.py --no-cpu-baseline --steps 200 --variant shvs 2>>$O/err.txt | tail -1 > $O/bench_shvs.jsonl

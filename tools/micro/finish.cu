@@ -1,0 +1,71 @@
+// microbenchmark: latency of finish_row (the per-row final stage of the top-k
+// kernel) in a 256-thread CTA, with the top-k kernel's launch bounds.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I include tools/micro/finish.cu -o tools/micro/finish
+#include <cstdio>
+#include <vector>
+#include "../../paper_2512_00719_b200/csrc/finish.cuh"
+using namespace dp;
+
+template <int MB>
+__global__ void __launch_bounds__(256, MB) kern(SampleArgs a, const float* row, int n, int plen, int nsel_in,
+                                                long long* cyc) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const FinLayout F = fin_layout(a.lcap);
+  __shared__ uint64_t sel[1024];
+  __shared__ FinishScratch fs;
+  const uint32_t t = threadIdx.x;
+  // candidate keys: the nsel largest of the row (by value)
+  for (int i = t; i < nsel_in; i += 256) sel[i] = comp_key(row[i], (uint32_t)i);
+  const dp_params_t p = a.params[0];
+  __syncthreads();
+  long long t0 = clock64();
+  for (int it = 0; it < 4; ++it) {
+    finish_row<float, kTail, 256>(a, 0, p, plen, row, 0, n, sel, nsel_in, 0.0, 0.0, smem, F, fs, t,
+                                  [] { __syncthreads(); });
+    __syncthreads();
+  }
+  long long t1 = clock64();
+  if (t == 0) cyc[0] = (t1 - t0) / 4;
+}
+
+int main() {
+  const int n = 8192, plen = 100, cap = 256, nsel = 150;
+  std::vector<float> h(n);
+  for (int i = 0; i < n; ++i) h[i] = (i < 1000) ? 5.0f - 0.004f * i : -3.0f - 1e-4f * i;
+  float* row; cudaMalloc(&row, n * 4); cudaMemcpy(row, h.data(), n * 4, cudaMemcpyHostToDevice);
+  std::vector<int> ids(cap), cnt(cap, 1);
+  for (int j = 0; j < plen; ++j) ids[j] = (j * 37) % n;
+  int *d_ids, *d_cnt, *d_len, *d_plen; cudaMalloc(&d_ids, cap * 4); cudaMalloc(&d_cnt, cap * 4);
+  cudaMalloc(&d_len, 4); cudaMalloc(&d_plen, 4);
+  cudaMemcpy(d_ids, ids.data(), cap * 4, cudaMemcpyHostToDevice); cudaMemcpy(d_cnt, cnt.data(), cap * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(d_len, &plen, 4, cudaMemcpyHostToDevice); cudaMemcpy(d_plen, &plen, 4, cudaMemcpyHostToDevice);
+  dp_params_t hp{}; hp.temperature = 0.8; hp.top_k = 50; hp.top_p = 0.9; hp.min_p = 0.05; hp.rep_penalty = 1.1;
+  hp.presence_penalty = 0.5; hp.frequency_penalty = 0.1; hp.seed = 0;
+  dp_params_t* d_p; cudaMalloc(&d_p, sizeof(hp)); cudaMemcpy(d_p, &hp, sizeof(hp), cudaMemcpyHostToDevice);
+  double hu[3] = {0.3, 0.5, 0.7}; double* d_u; cudaMalloc(&d_u, 24); cudaMemcpy(d_u, hu, 24, cudaMemcpyHostToDevice);
+  int32_t* tok; double* lp; uint8_t* fl; cudaMalloc(&tok, 4); cudaMalloc(&lp, 8); cudaMalloc(&fl, 1);
+  cudaMemset(fl, 0, 1);
+  long long* cyc; cudaMallocManaged(&cyc, 64);
+  long long* st; cudaMallocManaged(&st, 24 * 8);
+  SampleArgs a; memset(&a, 0, sizeof(a));
+  a.logits = row; a.ld = n; a.V = n; a.H = 0; a.params = d_p;
+  a.pen.ids = d_ids; a.pen.out_count = d_cnt; a.pen.len = d_len; a.pen.prompt_len = d_plen; a.pen.cap = cap;
+  a.pen.vocab_size = n; a.uniforms = d_u; a.n_rows = 1; a.token = tok; a.logprob = lp; a.flags = fl;
+  a.dbg.stats = (int64_t*)st;
+  a.kcap = 256; a.lcap = 512; a.wcap = 1024; a.split = 1; a.nt = 256;
+  const FinLayout F = fin_layout(a.lcap);
+  for (int mb : {1, 2, 4}) {
+    for (int rep = 0; rep < 2; ++rep) {
+      if (mb == 1) { cudaFuncSetAttribute(kern<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, F.bytes); kern<1><<<1, 256, F.bytes>>>(a, row, n, plen, nsel, cyc); }
+      if (mb == 2) { cudaFuncSetAttribute(kern<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, F.bytes); kern<2><<<1, 256, F.bytes>>>(a, row, n, plen, nsel, cyc); }
+      if (mb == 4) { cudaFuncSetAttribute(kern<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, F.bytes); kern<4><<<1, 256, F.bytes>>>(a, row, n, plen, nsel, cyc); }
+      cudaError_t e = cudaDeviceSynchronize();
+      if (e != cudaSuccess) { printf("err %s\n", cudaGetErrorString(e)); return 1; }
+    }
+    int tk; cudaMemcpy(&tk, tok, 4, cudaMemcpyDeviceToHost);
+    printf("  laps/row: 12 %lld 13 %lld 14 %lld 16 %lld 15 %lld\n", st[12] / 8, st[13] / 8, st[14] / 8, st[16] / 8, st[15] / 8);
+    for (int i = 0; i < 24; ++i) st[i] = 0;
+    printf("finish_row minBlocks=%d: %lld cycles (token %d)\n", mb, cyc[0], tk);
+  }
+  return 0;
+}

@@ -1,6 +1,7 @@
-"""Minimal driver for ncu captures: build a workload and run a few steps.
+"""Minimal driver for ncu captures: build a workload the way bench.py does and
+run a few sampling steps (no graph, no timing).
 
-    python tools/prof_step.py --config c2 --variant full --steps 3
+    python tools/prof_step.py --config c2 --variant full|shvs --steps 3
 """
 
 import argparse
@@ -24,6 +25,7 @@ def main():
     ap.add_argument("--variant", default="full")
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--split", type=int, default=0)
+    ap.add_argument("--kernel", type=int, default=0)
     ap.add_argument("--hot", type=int, default=16384)
     ap.add_argument("--bf16", action="store_true")
     args = ap.parse_args()
@@ -32,13 +34,18 @@ def main():
     prompts = [np.random.default_rng(s).integers(0, v, 32) for s in range(b)]
     src = SyntheticSource(v, device="cuda")
     hot = HotVocab(v, src.hot_ordering()[: args.hot]) if args.variant == "shvs" else None
-    plane = DecisionPlane(v, [SamplingParams(**cfg["params"])] * b, prompts=prompts, hot=hot, split=args.split,
+    params = [bench.row_params(cfg, s) for s in range(b)]
+    plane = DecisionPlane(v, params, prompts=prompts, hot=hot, split=args.split, kernel=args.kernel,
                           max_generated=136)
     perm = hot.device_maps(plane.device)[0] if hot is not None else None
-    dt = torch.bfloat16 if args.bf16 else torch.float32
+    dt = torch.bfloat16 if (args.bf16 or cfg["dtype"] == "bf16") else torch.float32
     x = src.generate(0, range(b), dtype=dt, perm=perm)
+    summ = plane.producer_summary(x) if args.variant == "shvs" else None
     for i in range(args.steps):
-        plane.sample(x, i, variant=args.variant)
+        if args.variant == "shvs":
+            plane.sample(x, i, variant="shvs", summary=summ, summary_raw=True)
+        else:
+            plane.sample(x, i)
     torch.cuda.synchronize()
     print("done")
 
