@@ -286,6 +286,82 @@ def _timed(g, dist=None, world=1):
     return ms
 
 
+def measure_shvs_e2e(args, cfg, plane_kw, src, seq_ids, dev, shard, world):
+    """SHVS (speculative hot-vocab sampling) on the same workload, the
+    paper's decision path: device step time (sample + penalty update, CUDA
+    graph) and end to end with HOST-resident hot-first logits — the hot prefix
+    is staged with one strided DMA, rejected rows' tails are read zero-copy
+    (dp_stage_hot + dp_sample_shvs_split).  The producer's penalty-free row
+    summary travels with the logits (make_shard_blocks contract,
+    service.py:470-504)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2512_00719_b200 import DecisionPlane, HotVocab
+
+    v, h = cfg["V"], args.hot
+    hot = HotVocab(v, src.hot_ordering()[:h])
+    plane = DecisionPlane(v, hot=hot, **plane_kw)
+    tdt = torch.float32 if cfg["dtype"] == "f32" else torch.bfloat16
+    esz = 4 if cfg["dtype"] == "f32" else 2
+    perm = hot.device_maps(dev)[0]
+    bufs = [src.generate(i, seq_ids, dtype=tdt, perm=perm) for i in range(2)]
+    summ = [plane.producer_summary(b) for b in bufs]
+    base_it = [args.warmup]
+
+    def step(i):
+        it = base_it[0] + i
+        if it % RESET_EVERY == 0 and it > 0:
+            plane.state.reset()
+        d = plane.sample(bufs[it & 1], it, variant="shvs", summary=summ[it & 1], summary_raw=True, update=False)
+        plane.state.update(d.token, d.flags)
+        return d
+
+    for i in range(args.warmup):
+        step(i - args.warmup)
+    torch.cuda.synchronize()
+    g = _graph(step, args.steps)
+    ms = _timed(g, dist if world > 1 else None, world)
+    d = plane.sample(bufs[0], 0, variant="shvs", summary=summ[0], summary_raw=True, update=False)
+    torch.cuda.synchronize()
+    flags = d.flags.cpu().numpy()
+    accept = float(np.mean((flags & 0x02) != 0))
+    rows = shard.rows
+    # e2e: pinned host logits -> stage hot prefix -> sample (tail zero-copy) -> D2H tokens
+    host = bufs[0].cpu().pin_memory()
+    sh = (summ[0][0].cpu().pin_memory(), summ[0][1].cpu().pin_memory())
+    staging = torch.empty((rows, h), dtype=tdt, device=dev)
+    tok_host = torch.empty(rows, dtype=torch.int32).pin_memory()
+    n_e2e = max(3, min(args.steps, 20))
+    st = torch.cuda.current_stream()
+    for k in range(2):   # warm the path
+        plane.sample_host(host, 20_000 + k, sh, staging=staging, summary_raw=True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    rej = 0
+    for k in range(n_e2e):
+        dd = plane.sample_host(host, 10_000 + k, sh, staging=staging, summary_raw=True)
+        tok_host.copy_(dd.token, non_blocking=True)
+    e1.record(st)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([e2e_ms, ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms, ms = float(t[0]), float(t[1])
+    rej = int(((dd.flags.cpu().numpy() & 0x08) != 0).sum())
+    tail_bytes = rej * (v - h) * esz
+    return {"hot_size": h, "accept": accept, "value": shard.batch_size * args.steps / (ms / 1000.0),
+            "ms_per_step": ms / args.steps,
+            "e2e": {"value": shard.batch_size * n_e2e / (e2e_ms / 1000.0), "unit": "tokens/s",
+                    "h2d_bytes_per_step": int(rows * h * esz + 16 * rows + tail_bytes),
+                    "d2h_bytes_per_step": int(rows * 4), "steps": n_e2e,
+                    "path": "DecisionPlane.sample_host: pinned hot-first host logits, hot prefix staged "
+                            "(dp_stage_hot), rejected tails read zero-copy (dp_sample_shvs_split); "
+                            "h2d counts the zero-copy tail bytes of the rejected rows"}}
+
+
 MIX = [  # C5: heterogeneous per-row params (BASELINE configs[4])
     dict(temperature=0.8, top_k=1),                                   # greedy
     dict(temperature=0.8, top_k=50),                                  # top-k only
@@ -479,6 +555,11 @@ def run_ours(args, cfg):
            "d2h_bytes_per_step": int(tok_host.numel() * 4), "steps": n_e2e,
            "path": "DecisionPlane.sample on pinned host logits (H2D + sample + D2H per step)"}
 
+    shvs = None
+    if variant == "full" and not args.no_shvs:
+        plane_kw = dict(params=params, prompts=prompts, seq_ids=seq_ids, device=dev, max_generated=RESET_EVERY + 8)
+        shvs = measure_shvs_e2e(args, cfg, plane_kw, src, seq_ids, dev, shard, world)
+
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
@@ -510,6 +591,7 @@ def run_ours(args, cfg):
                          "kernel_ms": kern_ms, "bytes_per_row": bytes_per_row},
             "producer_summary_ms": producer_ms,
             "shvs_accept": accept,
+            "shvs": shvs,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": args.steps * launches + sum(
@@ -537,6 +619,7 @@ def main():
     ap.add_argument("--ref-seconds", type=float, default=5.0)
     ap.add_argument("--ref-budget", type=float, default=90.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-shvs", action="store_true", help="skip the SHVS sub-measurement of the full-path line")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]

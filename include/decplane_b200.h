@@ -170,6 +170,30 @@ DP_API int dp_sample_shvs(const void* logits_hotfirst, int dtype, int64_t B, int
                    const dp_debug_t* debug_host, const dp_plan_t* plan_host,
                    int32_t* scratch_rows, void* stream);
 
+/* dp_sample_shvs over split storage: hot positions [0, H) of row b at
+ * logits_hot + b*ld_hot (device memory), tail positions [H, V) at
+ * logits_tail + b*ld_tail — device memory, or pinned (mapped) HOST memory that
+ * the tail pass reads zero-copy.  With host-resident logits a caller copies
+ * only the hot prefix to the GPU (the paper's hot/tail split, section 4.2):
+ * the tail crosses PCIe only for the rows the hot pass rejects.  Same
+ * decision law and outputs as dp_sample_shvs (shvs.py:198-255). */
+DP_API int dp_sample_shvs_split(const void* logits_hot, int64_t ld_hot, const void* logits_tail, int64_t ld_tail,
+                   int dtype, int64_t B, int64_t V, int64_t H, const int32_t* perm, const int32_t* inv_perm,
+                   const double* row_max, const double* total_expsum,
+                   const dp_params_t* params, const dp_penalty_t* pen_host,
+                   const double* uniforms, const uint64_t* seq_ids, uint64_t iteration,
+                   int32_t* token, double* logprob, uint8_t* flags,
+                   const dp_debug_t* debug_host, const dp_plan_t* plan_host,
+                   int32_t* scratch_rows, void* stream);
+
+/* Host-resident logits (the decision plane's CPU-side ring, transport.py:326-386):
+ * copy the hot prefix [0, H) of each hot-first host row (pinned, row stride
+ * ld_host elements) into a device staging buffer [B, ld_dev] — one strided
+ * DMA.  Pair with dp_sample_shvs_split(hot_dev, ld_dev, host_row + H, ld_host,
+ * ...) so only the hot prefix crosses PCIe up front. */
+DP_API int dp_stage_hot(const void* logits_host, int64_t ld_host, int dtype, int64_t B, int64_t H, void* hot_dev,
+                 int64_t ld_dev, void* stream);
+
 /* update_output_histogram (penalty.py:18-32) for every row: C_o[tok] += 1,
  * first-seen ids appended.  Rows whose flags[b] has DP_FLAG_DEGENERATE are
  * skipped; a full list sets DP_FLAG_PEN_OVERFLOW. flags may be NULL. */

@@ -236,18 +236,33 @@ int dp_row_summary_raw(const void* logits, int dtype, int64_t B, int64_t V, int6
                      "dp_row_summary_raw");
 }
 
-int dp_sample_shvs(const void* logits, int dtype, int64_t B, int64_t V, int64_t H, int64_t ld, const int32_t* perm,
-                   const int32_t* inv_perm, const double* row_max, const double* total_expsum,
-                   const dp_params_t* params, const dp_penalty_t* pen_host, const double* uniforms,
-                   const uint64_t* seq_ids, uint64_t iteration, int32_t* token, double* logprob, uint8_t* flags,
-                   const dp_debug_t* debug_host, const dp_plan_t* plan_host, int32_t* scratch_rows,
-                   void* stream) {
+}  // extern "C"
+
+namespace {
+// device-accessible address of a buffer that may be (mapped) pinned host memory
+const void* device_view(const void* p) {
+  cudaPointerAttributes at;
+  if (p && cudaPointerGetAttributes(&at, p) == cudaSuccess && at.type == cudaMemoryTypeHost) {
+    void* d = nullptr;
+    if (cudaHostGetDevicePointer(&d, const_cast<void*>(p), 0) == cudaSuccess) return d;
+    return at.devicePointer ? at.devicePointer : p;
+  }
+  cudaGetLastError();   // unregistered pageable pointers report an error: clear it
+  return p;
+}
+
+int sample_shvs_impl(const void* logits, int dtype, int64_t B, int64_t V, int64_t H, int64_t ld,
+                     const void* tail_logits, int64_t tail_ld, const int32_t* perm, const int32_t* inv_perm,
+                     const double* row_max, const double* total_expsum, const dp_params_t* params,
+                     const dp_penalty_t* pen_host, const double* uniforms, const uint64_t* seq_ids,
+                     uint64_t iteration, int32_t* token, double* logprob, uint8_t* flags,
+                     const dp_debug_t* debug_host, const dp_plan_t* plan_host, int32_t* scratch_rows, void* stream) {
   if (!logits || !params || !token || !logprob || !flags || !row_max || !total_expsum || !scratch_rows)
     return fail(DP_ERR_ARG, "dp_sample_shvs: null argument%s");
   if (!uniforms && !seq_ids) return fail(DP_ERR_ARG, "dp_sample_shvs: need uniforms or seq_ids%s");
   if (dtype != DP_F32 && dtype != DP_BF16) return fail(DP_ERR_UNSUPPORTED, "dp_sample_shvs: dtype%s");
-  if (B < 0 || V < 1 || H < 1 || H > V || ld < V || V >= (1ll << 31))
-    return fail(DP_ERR_ARG, "dp_sample_shvs: bad shape (need 1 <= H <= V <= ld)%s");
+  if (B < 0 || V < 1 || H < 1 || H > V || V >= (1ll << 31) || (tail_logits ? (ld < H || tail_ld < V - H) : ld < V))
+    return fail(DP_ERR_ARG, "dp_sample_shvs: bad shape (need 1 <= H <= V <= ld, or ld >= H and ld_tail >= V - H)%s");
   if ((perm == nullptr) != (inv_perm == nullptr)) return fail(DP_ERR_ARG, "dp_sample_shvs: perm/inv_perm%s");
   if (!valid_pen(pen_host, V)) return fail(DP_ERR_ARG, "dp_sample_shvs: penalty state does not match V%s");
   if (B == 0) return DP_OK;
@@ -258,6 +273,8 @@ int dp_sample_shvs(const void* logits, int dtype, int64_t B, int64_t V, int64_t 
   a.ld = ld;
   a.V = V;
   a.H = H;
+  a.tail_logits = tail_logits ? device_view(tail_logits) : nullptr;
+  a.tail_ld = tail_ld;
   a.perm = perm;
   a.inv_perm = inv_perm;
   a.params = params;
@@ -280,7 +297,7 @@ int dp_sample_shvs(const void* logits, int dtype, int64_t B, int64_t V, int64_t 
   a.reject_count = rej_count;
   // hot pass over [0, H)
   plan_topk(a, plan_host, B, H, dtype == DP_F32 ? 4 : 2);
-  const bool persistent = use_stream(B, plan_host);
+  const bool persistent = use_stream(B, plan_host) && !tail_logits;
   if (persistent) a.split = 1;
   const Launches L = plan_launches(a, plan_host, dp::kHot, B, H, persistent);
   if (L.warp && (e = dp::launch_warp(a, dtype, dp::kHot, (int)B, st)) != cudaSuccess)
@@ -314,6 +331,47 @@ int dp_sample_shvs(const void* logits, int dtype, int64_t B, int64_t V, int64_t 
   if (LT.general && (e = dp::launch_general(t, dtype, dp::kTail, (int)B, st)) != cudaSuccess)
     return cuda_status(e, "dp_sample_shvs/tail-general");
   return DP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dp_sample_shvs(const void* logits, int dtype, int64_t B, int64_t V, int64_t H, int64_t ld, const int32_t* perm,
+                   const int32_t* inv_perm, const double* row_max, const double* total_expsum,
+                   const dp_params_t* params, const dp_penalty_t* pen_host, const double* uniforms,
+                   const uint64_t* seq_ids, uint64_t iteration, int32_t* token, double* logprob, uint8_t* flags,
+                   const dp_debug_t* debug_host, const dp_plan_t* plan_host, int32_t* scratch_rows,
+                   void* stream) {
+  return sample_shvs_impl(logits, dtype, B, V, H, ld, nullptr, 0, perm, inv_perm, row_max, total_expsum, params,
+                          pen_host, uniforms, seq_ids, iteration, token, logprob, flags, debug_host, plan_host,
+                          scratch_rows, stream);
+}
+
+int dp_sample_shvs_split(const void* logits_hot, int64_t ld_hot, const void* logits_tail, int64_t ld_tail, int dtype,
+                         int64_t B, int64_t V, int64_t H, const int32_t* perm, const int32_t* inv_perm,
+                         const double* row_max, const double* total_expsum, const dp_params_t* params,
+                         const dp_penalty_t* pen_host, const double* uniforms, const uint64_t* seq_ids,
+                         uint64_t iteration, int32_t* token, double* logprob, uint8_t* flags,
+                         const dp_debug_t* debug_host, const dp_plan_t* plan_host, int32_t* scratch_rows,
+                         void* stream) {
+  if (!logits_tail && H < V) return fail(DP_ERR_ARG, "dp_sample_shvs_split: null tail%s");
+  return sample_shvs_impl(logits_hot, dtype, B, V, H, ld_hot, logits_tail ? logits_tail : logits_hot,
+                          logits_tail ? ld_tail : ld_hot, perm, inv_perm, row_max, total_expsum, params, pen_host,
+                          uniforms, seq_ids, iteration, token, logprob, flags, debug_host, plan_host, scratch_rows,
+                          stream);
+}
+
+int dp_stage_hot(const void* logits_host, int64_t ld_host, int dtype, int64_t B, int64_t H, void* hot_dev,
+                 int64_t ld_dev, void* stream) {
+  if (!logits_host || !hot_dev) return fail(DP_ERR_ARG, "dp_stage_hot: null argument%s");
+  if (dtype != DP_F32 && dtype != DP_BF16) return fail(DP_ERR_UNSUPPORTED, "dp_stage_hot: dtype%s");
+  if (B < 0 || H < 1 || ld_host < H || ld_dev < H) return fail(DP_ERR_ARG, "dp_stage_hot: bad shape%s");
+  if (B == 0) return DP_OK;
+  const size_t esz = dtype == DP_F32 ? 4 : 2;
+  return cuda_status(cudaMemcpy2DAsync(hot_dev, (size_t)ld_dev * esz, logits_host, (size_t)ld_host * esz,
+                                       (size_t)H * esz, (size_t)B, cudaMemcpyHostToDevice, (cudaStream_t)stream),
+                     "dp_stage_hot");
 }
 
 int dp_penalty_update(const dp_penalty_t* pen_host, const int32_t* token, int64_t B, uint8_t* flags, void* stream) {

@@ -291,7 +291,7 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
     double scorr = 0.0;   // raw producer summary -> penalized total (shvs.py:148-154 needs the ready row)
     if (a.summary_raw)
       scorr = raw_summary_correction(a, row, p, plen, mrow, t, NT,
-                                     [&](int64_t pos) { return Elem<T>::get(rowp - lo, pos); });
+                                     [&](int64_t pos) { return row_value<T>(a, row, pos); });
     spen = warp_sum(spen);
     scorr = warp_sum(scorr);
     if (lane == 0) {

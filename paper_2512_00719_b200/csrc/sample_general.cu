@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(kGenNT, 1) general_sample_kernel(SampleArgs a)
   const dp_params_t p = a.params[row];
   const int32_t plen_all = pen_len(a, row, p);
   if (route_row(a, MODE, p.top_k, plen_all, n) != kRouteGeneral) return;   // a streaming kernel's row
-  const T* rowp = reinterpret_cast<const T*>(a.logits) + (int64_t)row * a.ld + lo;
+  const T* rowp = domain_row<T>(a, row, MODE);
   const int32_t* pids = a.pen.ids + (int64_t)row * a.pen.cap;
   const int32_t* pcnt = a.pen.out_count + (int64_t)row * a.pen.cap;
   const double tau = p.temperature;
@@ -351,7 +351,7 @@ __global__ void __launch_bounds__(kGenNT, 1) general_sample_kernel(SampleArgs a)
     double corr = 0.0;
     if (a.summary_raw) {
       corr = raw_summary_correction(a, row, p, plen_all, mrow, tid, kGenNT,
-                                    [&](int64_t pos) { return Elem<T>::get(rowp - lo, pos); });
+                                    [&](int64_t pos) { return row_value<T>(a, row, pos); });
       corr = blk_sum_d(corr, g, sync);
     }
     const double S_prod = a.total_expsum[row];

@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_sample_kernel(Sample
       const dp_params_t p = a.params[row];
       const int32_t plen = pen_len(a, row, p);
       if (!topk_route<MODE>(a, p, plen, n)) continue;          // general-path row
-      const T* rowp = reinterpret_cast<const T*>(a.logits) + (int64_t)row * a.ld + lo;
+      const T* rowp = domain_row<T>(a, row, MODE);
       const uintptr_t addr = reinterpret_cast<uintptr_t>(rowp);
       const int64_t a0 = min64(n, (int64_t)(((16u - (addr & 15u)) & 15u) / sizeof(T)));
       const int32_t nvec = (int32_t)((n - a0) / EPV);
@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_sample_kernel(Sample
       const int row = R.row;
       if (row < 0) return;
       const dp_params_t p = a.params[row];
-      const T* rowp = reinterpret_cast<const T*>(a.logits) + (int64_t)row * a.ld + lo;
+      const T* rowp = domain_row<T>(a, row, MODE);
       uint64_t* ckey = cbuf(b);
       const uint32_t* bitmap = bmap(b);
       const int32_t a0 = R.a0;
@@ -352,7 +352,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_sample_kernel(Sample
       const dp_params_t p = a.params[row];
       const int32_t plen = pen_len(a, row, p);
       const uint32_t kp = (uint32_t)min64(n, (int64_t)p.top_k + (MODE == kHot ? 0 : plen));
-      rowp = reinterpret_cast<const T*>(a.logits) + (int64_t)row * a.ld + lo;
+      rowp = domain_row<T>(a, row, MODE);
       const uintptr_t addr = reinterpret_cast<uintptr_t>(rowp);
       a0 = (int32_t)min64(n, (int64_t)(((16u - (addr & 15u)) & 15u) / sizeof(T)));
       nvec = (int32_t)((n - a0) / EPV);

@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
   const uint32_t kp = (uint32_t)min64(n, (int64_t)k + (MODE == kHot ? 0 : plen));
   if (route_row(a, MODE, k, plen, n) != kRouteTopk) continue;   // another kernel's row (cluster-uniform)
 
-  const T* rowp = reinterpret_cast<const T*>(a.logits) + (int64_t)row * a.ld + lo;
+  const T* rowp = domain_row<T>(a, row, MODE);
   const int32_t* pids = a.pen.ids + (int64_t)row * a.pen.cap;
   const int32_t* pcnt = a.pen.out_count + (int64_t)row * a.pen.cap;
   const uint32_t ccap = L.ccap;

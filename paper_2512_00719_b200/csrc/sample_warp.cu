@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(kMW * 32, kMWBlocks) warp_sample_kernel(Sample
     const int32_t k = p.top_k;
     if (route_row(a, MODE, k, plen, n) != kRouteWarp) continue;   // CTA-uniform
     const uint32_t kp = (uint32_t)min64(n, (int64_t)k + plen);
-    const T* rowp = reinterpret_cast<const T*>(a.logits) + (int64_t)row * a.ld + lo;
+    const T* rowp = domain_row<T>(a, row, MODE);
     const int32_t* pids = a.pen.ids + (int64_t)row * a.pen.cap;
     const int32_t* pcnt = a.pen.out_count + (int64_t)row * a.pen.cap;
 
@@ -396,7 +396,7 @@ __global__ void __launch_bounds__(kMW * 32, kMWBlocks) warp_sample_kernel(Sample
         const int64_t pa = pa_r[i];   // absolute row position
         const int64_t q = pa - lo;
         const bool in = q >= 0 && q < n;
-        const float x = Elem<T>::get(rowp - lo, pa);
+        const float x = row_value<T>(a, row, pa);
         const double r = ready_penalized(x, pc_r[i], p);
         S.pq[j] = in ? (int32_t)q : -1;
         S.pkey[j] = f64_key(r);

@@ -34,11 +34,26 @@ struct SampleArgs {
   int32_t nt;                   // threads per CTA of the top-k kernel (128 / 256)
   int32_t summary_raw;          // kHot: row_max/total_expsum are the producer's raw summary
   int32_t use_warp;             // this call runs the warp-per-row kernel (sample_warp.cu)
+  const void* tail_logits;      // split SHVS storage: positions [H, V) of row b at
+  int64_t tail_ld;              //   tail_logits + b * tail_ld (device or mapped host memory)
 };
 
 DP_DEV int64_t dom_lo(const SampleArgs& a, int mode) { return mode == kTail ? a.H : 0; }
 DP_DEV int64_t dom_n(const SampleArgs& a, int mode) {
   return mode == kFull ? a.V : (mode == kHot ? a.H : a.V - a.H);
+}
+// the row's domain [dom_lo, dom_lo + dom_n) as a pointer to its first element
+template <typename T>
+DP_DEV const T* domain_row(const SampleArgs& a, int row, int mode) {
+  if (mode == kTail && a.tail_logits) return reinterpret_cast<const T*>(a.tail_logits) + (int64_t)row * a.tail_ld;
+  return reinterpret_cast<const T*>(a.logits) + (int64_t)row * a.ld + dom_lo(a, mode);
+}
+// raw logit at an absolute row position (either storage)
+template <typename T>
+DP_DEV float row_value(const SampleArgs& a, int row, int64_t pos) {
+  if (a.tail_logits && pos >= a.H)
+    return Elem<T>::get(reinterpret_cast<const T*>(a.tail_logits) + (int64_t)row * a.tail_ld, pos - a.H);
+  return Elem<T>::get(reinterpret_cast<const T*>(a.logits) + (int64_t)row * a.ld, pos);
 }
 DP_DEV int32_t pos_to_id(const SampleArgs& a, int64_t pos) {
   return a.perm ? __ldg(a.perm + pos) : (int32_t)pos;

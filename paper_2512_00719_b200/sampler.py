@@ -194,6 +194,63 @@ class DecisionPlane:
             self.state.update(d.token, d.flags)
         return d
 
+    def sample_split(self, hot, tail, iteration: int, summary, uniforms=None, update: bool = True,
+                     debug: bool = False, topk_stride: int = 0, summary_raw: bool = False) -> Decisions:
+        """SHVS over split storage: `hot` = [B, >=H] CUDA tensor with the hot
+        prefix of each hot-first row, `tail` = [B, >=V-H] tensor with the rest
+        — a CUDA tensor or a PINNED HOST tensor, read zero-copy by the tail pass
+        for rejected rows only.  `summary` = the producer's (row_max,
+        total_expsum) (required: the full row is not re-read here)."""
+        import torch
+
+        if self.hot is None:
+            raise ValueError("SHVS needs a HotVocab")
+        h = self.hot.size
+        if hot.dim() != 2 or hot.shape[0] != self.batch or hot.shape[1] < h or not hot.is_cuda or hot.stride(1) != 1:
+            raise ValueError(f"hot must be a CUDA tensor [{self.batch}, >= {h}] with unit stride")
+        if tail.dim() != 2 or tail.shape[0] != self.batch or tail.shape[1] < self.vocab_size - h or tail.stride(1) != 1:
+            raise ValueError(f"tail must be [{self.batch}, >= {self.vocab_size - h}] with unit stride")
+        if not tail.is_cuda and not tail.is_pinned():
+            raise ValueError("a host tail must be pinned memory (read zero-copy by the tail pass)")
+        if tail.dtype != hot.dtype:
+            raise ValueError("hot and tail must share a dtype")
+        dt = _dtype_code(hot)
+        d = self._outputs(debug, topk_stride)
+        dbg = self._debug_struct(d, topk_stride, debug)
+        perm, inv = self.hot.device_maps(self.device)
+        rmax, tot = summary
+        self._plan.summary_raw = 1 if summary_raw else 0
+        N.call("dp_sample_shvs_split", _ptr(hot), hot.stride(0), _ptr(tail), tail.stride(0), dt, self.batch,
+               self.vocab_size, h, _ptr(perm), _ptr(inv), _ptr(rmax), _ptr(tot), _ptr(self._params_dev),
+               C.byref(self.state.native), _ptr(uniforms), _ptr(self._seq_dev), int(iteration), _ptr(d.token),
+               _ptr(d.logprob), _ptr(d.flags), C.byref(dbg), C.byref(self._plan), _ptr(self._scratch), _stream())
+        if update:
+            self.state.update(d.token, d.flags)
+        return d
+
+    def sample_host(self, logits_host, iteration: int, summary_host, staging=None, update: bool = True,
+                    summary_raw: bool = False) -> Decisions:
+        """SHVS on HOST-resident hot-first logits (pinned [B, V] tensor): the hot
+        prefix is staged to the GPU with one strided DMA (dp_stage_hot), the
+        tail is read zero-copy by the tail pass for rejected rows only
+        (dp_sample_shvs_split).  `summary_host` = the producer's (row_max,
+        total_expsum), host f64 [B] tensors (copied with the logits)."""
+        import torch
+
+        if self.hot is None:
+            raise ValueError("SHVS needs a HotVocab")
+        if logits_host.is_cuda or not logits_host.is_pinned() or logits_host.stride(1) != 1:
+            raise ValueError("logits_host must be a pinned host tensor with unit stride along V")
+        h = self.hot.size
+        if staging is None or staging.shape != (self.batch, h) or staging.dtype != logits_host.dtype:
+            staging = torch.empty((self.batch, h), dtype=logits_host.dtype, device=self.device)
+        N.call("dp_stage_hot", _ptr(logits_host), logits_host.stride(0), _dtype_code(logits_host), self.batch, h,
+               _ptr(staging), staging.stride(0), _stream())
+        rmax = summary_host[0].to(self.device, non_blocking=True)
+        tot = summary_host[1].to(self.device, non_blocking=True)
+        tail = logits_host[:, h:]
+        return self.sample_split(staging, tail, iteration, (rmax, tot), update=update, summary_raw=summary_raw)
+
     def row_summary(self, logits, inv_perm=None):
         """(row_max, total_expsum) of the ready rows (service.py:484-489)."""
         import torch

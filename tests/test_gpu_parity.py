@@ -59,7 +59,7 @@ def compare(tag, gpu_tok, gpu_lp, dec, exempt_log):
     assert not bad, f"{tag}: token mismatches outside the boundary band: {bad[:8]}"
 
 
-def run_golden(torch, name, variant, raw_summary=False, kernel=0):
+def run_golden(torch, name, variant, raw_summary=False, kernel=0, storage="whole"):
     case = Case(name)
     params = case.params()
     states = case.states()
@@ -76,7 +76,19 @@ def run_golden(torch, name, variant, raw_summary=False, kernel=0):
         if variant == "shvs":
             xt = plane.hot.to_hot_first(xt).contiguous()
         summ = plane.producer_summary(xt) if raw_summary else None
-        d = plane.sample(xt, it, variant=variant, debug=True, summary=summ, summary_raw=raw_summary)
+        if storage == "whole":
+            d = plane.sample(xt, it, variant=variant, debug=True, summary=summ, summary_raw=raw_summary)
+        else:
+            # split storage: hot prefix on the device, tail on the device or in
+            # pinned host memory (read zero-copy by the tail pass)
+            h = plane.hot.size
+            if summ is None:
+                summ = plane.row_summary(xt, inv_perm=plane.hot.device_maps(plane.device)[1])
+            hot = xt[:, :h].contiguous()
+            tail = xt[:, h:].contiguous()
+            if storage == "split_host":
+                tail = tail.cpu().pin_memory()
+            d = plane.sample_split(hot, tail, it, summ, debug=True, summary_raw=raw_summary)
         tok, lp = d.token.cpu().numpy(), d.logprob.cpu().numpy()
         compare(f"{name}/it{it}", tok, lp, dec, exempt)
         fl = d.flags.cpu().numpy()
@@ -293,3 +305,12 @@ def test_adversarial_rows_match_oracle(torch_cuda, kernel):
             states[b].update(int(dec[b].token))
         plane.state.update(torch.from_numpy(np.array([dd.token for dd in dec], np.int32)).cuda())
     print("exemptions:", exempt)
+
+
+@pytest.mark.parametrize("storage", ["split_dev", "split_host"])
+@pytest.mark.parametrize("raw", [False, True])
+@pytest.mark.parametrize("name", ["shvs_accept", "shvs_reject", "het_shvs"])
+def test_shvs_split_storage(torch_cuda, name, raw, storage):
+    """dp_sample_shvs_split: hot prefix in device memory, tail in device or
+    pinned host memory (zero-copy) — the same decisions as the reference."""
+    run_golden(torch_cuda, name, "shvs", raw_summary=raw, storage=storage)

@@ -26,6 +26,25 @@ __global__ void __launch_bounds__(256, MB) kern(SampleArgs a, const float* row, 
   }
   long long t1 = clock64();
   if (t == 0) cyc[0] = (t1 - t0) / 4;
+  // the draw alone, on the final list finish_row left in shared memory
+  double* fr = reinterpret_cast<double*>(smem + F.r);
+  double* fw = reinterpret_cast<double*>(smem + F.w);
+  double* fc = reinterpret_cast<double*>(smem + F.cum);
+  __syncthreads();
+  if (t < 32) {
+    double acc = 0;
+    long long d0 = clock64();
+    for (int it = 0; it < 10; ++it) {
+      DrawResult d = warp_filter_draw(fr, p.top_k, p, 0.3 + 1e-3 * it, fw, fc, a.dbg.stats);
+      acc += d.logprob;
+    }
+    long long d1 = clock64();
+    if (t == 0) { cyc[1] = (d1 - d0) / 10; cyc[3] = (long long)acc; }
+    d0 = clock64();
+    DrawResult d = warp_filter_draw(fr, p.top_k, p, 0.77, fw, fc, a.dbg.stats);
+    d1 = clock64();
+    if (t == 0) { cyc[2] = d1 - d0; cyc[4] = d.index; }
+  }
 }
 
 int main() {
@@ -65,7 +84,7 @@ int main() {
     int tk; cudaMemcpy(&tk, tok, 4, cudaMemcpyDeviceToHost);
     printf("  laps/row: 12 %lld 13 %lld 14 %lld 16 %lld 15 %lld\n", st[12] / 8, st[13] / 8, st[14] / 8, st[16] / 8, st[15] / 8);
     for (int i = 0; i < 24; ++i) st[i] = 0;
-    printf("finish_row minBlocks=%d: %lld cycles (token %d)\n", mb, cyc[0], tk);
+    printf("finish_row minBlocks=%d: %lld cycles (token %d); draw in loop %lld, draw once %lld\n", mb, cyc[0], tk, cyc[1], cyc[2]);
   }
   return 0;
 }
