@@ -39,6 +39,10 @@ CONFIGS = {
     "c4": dict(V=151936, B=8192, dtype="f32", params=C2_PARAMS, name="qwen3-151936-b8192", strong=True),
     "c5": dict(V=152064, B=16384, dtype="bf16", params=C2_PARAMS, name="qwen2.5-152k-b16384-bf16-mix",
                mix=True),
+    # diagnostics (not BASELINE configs): C2 shape, one filter kind per run
+    "c2p": dict(V=152064, B=1024, dtype="f32", params=dict(temperature=0.8, top_p=0.9), name="c2-top-p-only"),
+    "c2m": dict(V=152064, B=1024, dtype="f32", params=dict(temperature=0.8, min_p=0.05), name="c2-min-p-only"),
+    "c2n": dict(V=152064, B=1024, dtype="f32", params=dict(temperature=0.8), name="c2-neutral"),
 }
 METRIC = "sampled tokens/s at V=152k, B=1024; achieved HBM GB/s vs B200 peak"
 PROMPT_LEN = 32
@@ -416,6 +420,7 @@ def run_ours(args, cfg):
     hot = HotVocab(v, src.hot_ordering()[: args.hot]) if variant == "shvs" else None
     plane = DecisionPlane(v, params, prompts=prompts, seq_ids=seq_ids, hot=hot, device=dev,
                           max_generated=RESET_EVERY + 8, split=args.split, kernel=args.kernel)
+    plane._plan.threads = args.threads
     tdt = torch.float32 if cfg["dtype"] == "f32" else torch.bfloat16
     perm = hot.device_maps(dev)[0] if hot is not None else None
     bufs = [src.generate(i, seq_ids, dtype=tdt, perm=perm) for i in range(2)]   # 2 x batch > L2
@@ -615,6 +620,7 @@ def main():
     ap.add_argument("--variant", default="full", choices=["full", "shvs"])
     ap.add_argument("--split", type=int, default=0)
     ap.add_argument("--kernel", type=int, default=0, help="dp_plan_t.kernel: 0 auto, 1 CTA/cluster, 2 warp-per-row")
+    ap.add_argument("--threads", type=int, default=0, help="dp_plan_t.threads of the top-k kernel (0/256 or 128)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-seconds", type=float, default=5.0)
     ap.add_argument("--ref-budget", type=float, default=90.0)

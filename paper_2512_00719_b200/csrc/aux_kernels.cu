@@ -32,11 +32,21 @@ __global__ void penalty_update_kernel(dp_penalty_t pen, const int32_t* token, in
   int32_t* ids = pen.ids + row * pen.cap;
   int32_t* cnt = pen.out_count + row * pen.cap;
   const int32_t len = pen.len[row];
+  // all loads of a 256-entry window in flight at once (one memory round trip
+  // for the usual list sizes), then the first match
   int32_t hit = -1;
-  for (int32_t base = 0; base < len && hit < 0; base += 32) {
-    const int32_t j = base + lane;
-    const uint32_t m = __ballot_sync(0xffffffffu, j < len && ids[j] == tok);
-    if (m) hit = base + __ffs(m) - 1;
+  for (int32_t base = 0; base < len && hit < 0; base += 256) {
+    int32_t v[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int32_t j = base + r * 32 + (int32_t)lane;
+      v[r] = j < len ? ids[j] : -1;
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const uint32_t m = __ballot_sync(0xffffffffu, v[r] == tok);
+      if (m && hit < 0) hit = base + r * 32 + __ffs(m) - 1;
+    }
   }
   if (lane == 0) {
     if (hit >= 0) {

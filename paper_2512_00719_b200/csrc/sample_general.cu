@@ -181,13 +181,15 @@ __global__ void __launch_bounds__(kGenNT, 1) general_sample_kernel(SampleArgs a)
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u;
   auto sync = [] { __syncthreads(); };
 
-  const int ridx = blockIdx.x;
   const int nrows = a.row_count ? *a.row_count : a.n_rows;
-  if (ridx >= nrows) return;
+  // CTAs loop over the rows (grid sized to the resident CTAs): rows routed to
+  // the streaming kernels cost one parameter read here
+  for (int ridx = blockIdx.x; ridx < nrows; ridx += gridDim.x) {
   const int row = a.rows ? a.rows[ridx] : ridx;
   const dp_params_t p = a.params[row];
   const int32_t plen_all = pen_len(a, row, p);
-  if (route_row(a, MODE, p.top_k, plen_all, n) != kRouteGeneral) return;   // a streaming kernel's row
+  if (route_row(a, MODE, p.top_k, plen_all, n) != kRouteGeneral) continue;   // a streaming kernel's row
+  sync();   // the previous row is done with the shared buffers
   const T* rowp = domain_row<T>(a, row, MODE);
   const int32_t* pids = a.pen.ids + (int64_t)row * a.pen.cap;
   const int32_t* pcnt = a.pen.out_count + (int64_t)row * a.pen.cap;
@@ -235,7 +237,7 @@ __global__ void __launch_bounds__(kGenNT, 1) general_sample_kernel(SampleArgs a)
       a.logprob[row] = 0.0;
       a.flags[row] = DP_FLAG_DEGENERATE;
     }
-    return;
+    continue;
   }
   // raw-unit anchor of the weights: w = exp((x - c)/tau), c = rmax*tau (hi/lo)
   const double cd = rmax * tau;
@@ -380,7 +382,7 @@ __global__ void __launch_bounds__(kGenNT, 1) general_sample_kernel(SampleArgs a)
           a.logprob[row] = 0.0;
         }
       }
-      return;
+      continue;
     }
   }
 
@@ -639,6 +641,7 @@ __global__ void __launch_bounds__(kGenNT, 1) general_sample_kernel(SampleArgs a)
     if (a.dbg.bytes_touched)
       a.dbg.bytes_touched[row] = (MODE == kTail ? a.dbg.bytes_touched[row] : 0ull) + (uint64_t)n * sizeof(T);
   }
+  }
 }
 
 template <typename T, int MODE>
@@ -649,7 +652,13 @@ static cudaError_t launch_general_t(const SampleArgs& a, int grid_rows, cudaStre
   auto kern = general_sample_kernel<T, MODE>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  kern<<<grid_rows, kGenNT, smem, st>>>(a);
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kGenNT, smem) != cudaSuccess || per_sm < 1) per_sm = 1;
+  const int grid = grid_rows < sms * per_sm ? grid_rows : sms * per_sm;
+  if (grid < 1) return cudaSuccess;
+  kern<<<grid, kGenNT, smem, st>>>(a);
   return cudaGetLastError();
 }
 

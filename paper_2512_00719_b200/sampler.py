@@ -251,6 +251,28 @@ class DecisionPlane:
         tail = logits_host[:, h:]
         return self.sample_split(staging, tail, iteration, (rmax, tot), update=update, summary_raw=summary_raw)
 
+    def hot_mass_curve(self, logits_hotfirst, grid, summary=None):
+        """Per-row hot mass alpha(H) at every grid size H (ready mass of the
+        first H hot positions / total), [B, G] f64 on device — the batched
+        GPU form of sizing.estimate_hit_ratio_curve (sizing.py:78-100)."""
+        import torch
+
+        if self.hot is None:
+            raise ValueError("the hit-ratio curve needs a HotVocab")
+        g = sorted(int(h) for h in grid)
+        if not g or g[0] < 1 or g[-1] > self.vocab_size:
+            raise ValueError(f"grid sizes must lie in [1, {self.vocab_size}]")
+        perm, inv = self.hot.device_maps(self.device)
+        if summary is None:
+            summary = self.row_summary(logits_hotfirst, inv_perm=inv)
+        rmax, tot = summary
+        gd = torch.tensor(g, dtype=torch.int32, device=self.device)
+        out = torch.empty((self.batch, len(g)), dtype=torch.float64, device=self.device)
+        N.call("dp_hot_mass_curve", _ptr(logits_hotfirst), _dtype_code(logits_hotfirst), self.batch,
+               self.vocab_size, logits_hotfirst.stride(0), _ptr(rmax), _ptr(tot), _ptr(self._params_dev),
+               C.byref(self.state.native), _ptr(inv), _ptr(gd), len(g), _ptr(out), _stream())
+        return out
+
     def row_summary(self, logits, inv_perm=None):
         """(row_max, total_expsum) of the ready rows (service.py:484-489)."""
         import torch

@@ -314,3 +314,28 @@ def test_shvs_split_storage(torch_cuda, name, raw, storage):
     """dp_sample_shvs_split: hot prefix in device memory, tail in device or
     pinned host memory (zero-copy) — the same decisions as the reference."""
     run_golden(torch_cuda, name, "shvs", raw_summary=raw, storage=storage)
+
+
+def test_hot_mass_curve_matches_oracle(torch_cuda):
+    """K6 (dp_hot_mass_curve): alpha(H) per row on hot-first rows with
+    penalties == the reference hit-ratio estimate on the ready softmax
+    (sizing.estimate_hit_ratio_curve, sizing.py:78-100)."""
+    torch = torch_cuda
+    v, bsz = 4096, 8
+    params = [O.Params(temperature=0.8, top_k=50, rep_penalty=1.2, presence_penalty=0.3, seed=b)
+              for b in range(bsz)]
+    prompts = [np.random.default_rng(b).integers(0, v, 24) for b in range(bsz)]
+    src = O.Synthetic(v)
+    hot_ids = src.rank_to_token[:1024]
+    plane = plane_for(torch, v, params, prompts, hot_ids=hot_ids)
+    x = src.wire(2, range(bsz))
+    xt = plane.hot.to_hot_first(torch.from_numpy(x).cuda()).contiguous()
+    grid = [1, 64, 256, 512, 1024]
+    got = plane.hot_mass_curve(xt, grid).cpu().numpy()
+    states = [O.State.new(p, v) for p in prompts]
+    for b in range(bsz):
+        r = O.ready_row(x[b], states[b], params[b])
+        w = np.exp(r - r.max())
+        prob = w / w.sum()
+        want = np.cumsum(prob[hot_ids])[np.array(grid) - 1]
+        np.testing.assert_allclose(got[b], np.minimum(want, 1.0), rtol=1e-6, atol=1e-12)
