@@ -62,6 +62,44 @@ int32_t* work_counter(int slot) {
   }
   return g_work[dev] + slot;
 }
+// Per-device fallback row lists for nucleus rows (slot 0: full, 1: SHVS hot,
+// 2: SHVS tail): [count, rows...], grown on demand.  Allocated by the first
+// (eager) call of a batch size; stream-ordered reuse like work_counter.
+int32_t* fallback_list(int slot, int64_t B) {
+  static int32_t* g_buf[64][3] = {{nullptr}};
+  static int64_t g_cap[64][3] = {{0}};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  if (g_cap[dev][slot] < B + 1) {
+    int32_t* p = nullptr;
+    if (cudaMalloc(&p, (size_t)(B + 1) * sizeof(int32_t)) != cudaSuccess) return nullptr;
+    if (g_buf[dev][slot]) cudaFree(g_buf[dev][slot]);
+    g_buf[dev][slot] = p;
+    g_cap[dev][slot] = B + 1;
+  }
+  return g_buf[dev][slot];
+}
+// some row may have top-k off (the plan's lower bound does not exclude it)
+bool nucleus_possible(const dp_plan_t* plan) { return !(plan && plan->min_top_k > 0); }
+// arm the fallback list of a call (nucleus rows routed to the top-k kernel)
+cudaError_t arm_fallback(dp::SampleArgs& a, int slot, int64_t B, cudaStream_t st) {
+  int32_t* fb = fallback_list(slot, B);
+  if (!fb) return cudaErrorMemoryAllocation;
+  a.fb_count = fb;
+  a.fb_rows = fb + 1;
+  return cudaMemsetAsync(fb, 0, sizeof(int32_t), st);
+}
+// the general kernel over the fallback list (after the top-k kernel)
+cudaError_t launch_fallback(const dp::SampleArgs& a, int dtype, int mode, int64_t B, cudaStream_t st) {
+  dp::SampleArgs g = a;
+  g.rows = a.fb_rows;
+  g.row_count = a.fb_count;
+  g.fb_rows = nullptr;
+  g.fb_count = nullptr;
+  g.force_general = 1;
+  return dp::launch_general(g, dtype, mode, (int)B, st);
+}
+
 // the persistent TMA-ring kernel is opt-in (plan->split == -1) until it beats
 // the per-row CTA kernel; see sample_stream.cu
 bool use_stream(int64_t B, const dp_plan_t* plan) {
@@ -111,7 +149,8 @@ bool valid_pen(const dp_penalty_t* pen, int64_t V) {
 
 // capacities for the streaming top-k kernel (see sample_topk.cu)
 void plan_topk(dp::SampleArgs& a, const dp_plan_t* plan, int64_t B, int64_t n, int elem_bytes) {
-  const int32_t kmax = (plan && plan->max_top_k > 0) ? plan->max_top_k : 256;
+  int32_t kmax = (plan && plan->max_top_k > 0) ? plan->max_top_k : 256;
+  if (nucleus_possible(plan) && kmax < dp::kNucK) kmax = dp::kNucK;   // nucleus rows keep kNucK
   const uint32_t kcap = pow2_at_least((uint32_t)kmax + (uint32_t)a.pen.cap);
   a.kcap = (int32_t)(kcap < 32u ? 32u : kcap);
   if (a.kcap > 2048) a.kcap = 2048;
@@ -198,14 +237,18 @@ int dp_sample_full(const void* logits, int dtype, int64_t B, int64_t V, int64_t 
   plan_topk(a, plan_host, B, V, dtype == DP_F32 ? 4 : 2);
   const bool persistent = use_stream(B, plan_host);
   if (persistent) a.split = 1;
-  const Launches L = plan_launches(a, plan_host, dp::kFull, B, V, persistent);
   cudaError_t e = cudaSuccess;
+  const bool nuc = nucleus_possible(plan_host) && !persistent;
+  if (nuc && (e = arm_fallback(a, 0, B, st)) != cudaSuccess) return cuda_status(e, "dp_sample_full/fallback");
+  const Launches L = plan_launches(a, plan_host, dp::kFull, B, V, persistent);
   if (L.warp && (e = dp::launch_warp(a, dtype, dp::kFull, (int)B, st)) != cudaSuccess)
     return cuda_status(e, "dp_sample_full/warp");
   if (L.topk && (e = launch_sampler(a, dtype, dp::kFull, B, persistent, 0, st)) != cudaSuccess)
     return cuda_status(e, "dp_sample_full/topk");
   if (L.general && (e = dp::launch_general(a, dtype, dp::kFull, (int)B, st)) != cudaSuccess)
     return cuda_status(e, "dp_sample_full/general");
+  if (nuc && (e = launch_fallback(a, dtype, dp::kFull, B, st)) != cudaSuccess)
+    return cuda_status(e, "dp_sample_full/fallback");
   return DP_OK;
 }
 
@@ -299,6 +342,8 @@ int sample_shvs_impl(const void* logits, int dtype, int64_t B, int64_t V, int64_
   plan_topk(a, plan_host, B, H, dtype == DP_F32 ? 4 : 2);
   const bool persistent = use_stream(B, plan_host) && !tail_logits;
   if (persistent) a.split = 1;
+  const bool nuc = nucleus_possible(plan_host) && !persistent;
+  if (nuc && (e = arm_fallback(a, 1, B, st)) != cudaSuccess) return cuda_status(e, "dp_sample_shvs/fallback");
   const Launches L = plan_launches(a, plan_host, dp::kHot, B, H, persistent);
   if (L.warp && (e = dp::launch_warp(a, dtype, dp::kHot, (int)B, st)) != cudaSuccess)
     return cuda_status(e, "dp_sample_shvs/hot-warp");
@@ -306,6 +351,8 @@ int sample_shvs_impl(const void* logits, int dtype, int64_t B, int64_t V, int64_
     return cuda_status(e, "dp_sample_shvs/hot-topk");
   if (L.general && (e = dp::launch_general(a, dtype, dp::kHot, (int)B, st)) != cudaSuccess)
     return cuda_status(e, "dp_sample_shvs/hot-general");
+  if (nuc && (e = launch_fallback(a, dtype, dp::kHot, B, st)) != cudaSuccess)
+    return cuda_status(e, "dp_sample_shvs/hot-fallback");
   if (H == V) return DP_OK;
   // tail pass over [H, V) for the rows the hot pass rejected
   dp::SampleArgs t = a;
@@ -313,6 +360,7 @@ int sample_shvs_impl(const void* logits, int dtype, int64_t B, int64_t V, int64_
   t.row_count = rej_count;
   t.reject_rows = nullptr;
   t.reject_count = nullptr;
+  if (nuc && (e = arm_fallback(t, 2, B, st)) != cudaSuccess) return cuda_status(e, "dp_sample_shvs/fallback");
   plan_topk(t, plan_host, B, V - H, dtype == DP_F32 ? 4 : 2);
   // The tail pass serves only the rejected rows (typically a few percent of
   // B, count known on the device only): 8-CTA clusters split each row over 8
@@ -330,6 +378,8 @@ int sample_shvs_impl(const void* logits, int dtype, int64_t B, int64_t V, int64_
     return cuda_status(e, "dp_sample_shvs/tail-topk");
   if (LT.general && (e = dp::launch_general(t, dtype, dp::kTail, (int)B, st)) != cudaSuccess)
     return cuda_status(e, "dp_sample_shvs/tail-general");
+  if (nuc && (e = launch_fallback(t, dtype, dp::kTail, B, st)) != cudaSuccess)
+    return cuda_status(e, "dp_sample_shvs/tail-fallback");
   return DP_OK;
 }
 

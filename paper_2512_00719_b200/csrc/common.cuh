@@ -199,6 +199,7 @@ DP_DEV void st_dsmem_u64(uint32_t addr, uint64_t v) {
 DP_DEV void st_dsmem_u32(uint32_t addr, uint32_t v) {
   asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
+DP_DEV void st_dsmem_f32(uint32_t addr, float v) { st_dsmem_u32(addr, __float_as_uint(v)); }
 DP_DEV void st_dsmem_f64(uint32_t addr, double v) {
   asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
 }

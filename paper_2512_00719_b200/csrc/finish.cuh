@@ -235,9 +235,13 @@ template <typename T, int MODE, int NT, typename Sync>
 DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32_t plen, const T* rowp,
                        int64_t lo, int64_t n, const uint64_t* sel, uint32_t nsel, double sh_unpen, double mrow,
                        uint8_t* fin, const FinLayout& F, FinishScratch& fs, uint32_t t, Sync sync,
-                       const PenPrefetch* pp = nullptr) {
+                       const PenPrefetch* pp = nullptr, float cref = 0.f) {
   const uint32_t warp = t >> 5, lane = t & 31u;
-  const int32_t k = p.top_k;
+  // nucleus rows (top-k off): the list holds the kNucK largest; sh_unpen is
+  // the domain mass (kHot: hot mass relative to mrow; kFull / kTail: every
+  // element's f32 term relative to cref, penalized ones swapped below)
+  const bool nuc = nucleus_row(p.top_k, n);
+  const int32_t k = effective_k(p.top_k, n);
   const int32_t* pids = a.pen.ids + (int64_t)row * a.pen.cap;
   const int32_t* pcnt = a.pen.out_count + (int64_t)row * a.pen.cap;
   uint64_t* fkey = reinterpret_cast<uint64_t*>(fin + F.key);
@@ -280,6 +284,7 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
   // kHot: alpha and the accept test first (shvs.py:223-236)
   double alpha = 1.0;
   bool imprecise = false;
+  double s_dom = sh_unpen;   // nucleus: mass of the whole domain (see above)
   if (MODE == kHot) {
     double spen = 0.0;   // exact mass of penalized hot ids (f64)
     for (int32_t j = t; j < plen; j += NT) {
@@ -304,6 +309,7 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
       sH += fs.sh_pen[w];
       corr += fs.corr[w];
     }
+    s_dom = sH;
     const double S_prod = a.total_expsum[row];
     const double S = S_prod + corr;
     // a raw summary dominated by since-penalized mass loses relative precision
@@ -342,6 +348,10 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
   if (MODE != kHot)
     for (uint32_t i = t; i < hcap; i += NT) hash[i] = 0xFFFFFFFFu;
   sync();
+  const bool nuc_mass = nuc && MODE != kHot;
+  const float s2 = (float)(1.4426950408889634 / p.temperature);
+  const double cref_r = (double)cref / p.temperature;   // cref in ready units
+  double m_sub = 0.0, m_add = 0.0;
   for (int32_t j = t; j < plen; j += NT) {
     int32_t pos, c;
     float x;
@@ -351,12 +361,28 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
         uint32_t h = ((uint32_t)pos * 2654435761u) & hmask;
         while (atomicCAS(&hash[h], 0xFFFFFFFFu, (uint32_t)pos) != 0xFFFFFFFFu) h = (h + 1u) & hmask;
       }
+      const double r = ready_penalized(x, c, p);
       const uint32_t s = atomicAdd(&fs.nl, 1u);
-      fkey[s] = f64_key(ready_penalized(x, c, p));
+      fkey[s] = f64_key(r);
       fpos[s] = (uint32_t)pos;
+      if (nuc_mass) {   // swap the streamed f32 term (bit-identical) for the exact one
+        m_sub += (double)ex2_fast(((x - cref) - 0.f) * s2);
+        m_add += exp(r - cref_r);
+      }
+    }
+  }
+  if (nuc_mass) {
+    m_sub = warp_sum(m_sub);
+    m_add = warp_sum(m_add);
+    if (lane == 0) {
+      fs.sh_pen[warp] = m_sub;
+      fs.corr[warp] = m_add;
     }
   }
   sync();
+  if (nuc_mass) {
+    for (int w = 0; w < NT / 32; ++w) s_dom += fs.corr[w] - fs.sh_pen[w];   // fixed order
+  }
   lap(12);
   for (uint32_t i = t; i < nsel; i += NT) {
     const uint64_t key = sel[i];
@@ -427,9 +453,22 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
 
   lap(14);
   if (warp == 0) {
-    const DrawResult d = warp_filter_draw(fr, k, p, u[MODE == kTail ? 2 : 0], fw, fcum, a.dbg.stats);
+    const double ud = u[MODE == kTail ? 2 : 0];
+    bool fb = false;
+    DrawResult d;
+    if (nuc) {
+      // domain mass relative to the top ready value r[0]
+      const double ref = MODE == kHot ? mrow : cref_r;
+      const double total = s_dom * exp(ref - fr[0]);
+      if (!(total > 0.0) || !isfinite(total)) fb = true;   // e.g. the first batch missed the row's scale
+      else d = warp_filter_draw_nuc(fr, (int32_t)min((uint32_t)k, nl), p, ud, total, fw, fcum, fb);
+    } else {
+      d = warp_filter_draw(fr, k, p, ud, fw, fcum, a.dbg.stats);
+    }
     lap(16);
-    if (lane == 0) {
+    if (fb) {
+      if (lane == 0) a.fb_rows[atomicAdd(a.fb_count, 1)] = row;   // the general kernel decides it
+    } else if (lane == 0) {
       const int64_t pos = (int64_t)fpos[d.index] + lo;
       a.token[row] = pos_to_id(a, pos);
       a.logprob[row] = d.logprob;
@@ -445,7 +484,7 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
       if (a.dbg.bytes_touched)
         a.dbg.bytes_touched[row] = (MODE == kTail ? a.dbg.bytes_touched[row] : 0ull) + (uint64_t)n * sizeof(T);
     }
-    if (a.dbg.topk_ids) {
+    if (a.dbg.topk_ids && !fb) {
       const int32_t m = min(k, a.dbg.topk_stride);
       for (int32_t j = lane; j < m; j += 32) {
         a.dbg.topk_ids[(int64_t)row * a.dbg.topk_stride + j] = pos_to_id(a, (int64_t)fpos[j] + lo);

@@ -40,7 +40,9 @@ struct TopkSmem {
   static constexpr int NW = NT / 32;
   uint64_t mbar;              // CTA 0: arrivals of the other cluster CTAs
   double sh_warp[NW];
-  double sh_recv[8];          // CTA 0: per-rank hot mass
+  double sh_recv[8];          // CTA 0: per-rank hot mass (kHot) / nucleus mass
+  float c_recv[8];            // CTA 0: per-rank nucleus mass reference
+  float max_warp[NW];
   double sh_pen[NW];
   float thr_warp[NW];
   float est_warp[NW];
@@ -113,8 +115,14 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
   const dp_params_t p = a.params[row];
   const int32_t plen = pen_len(a, row, p);
   const int32_t k = p.top_k;
+  // nucleus rows (top-k off) keep the kNucK largest plus the domain mass;
+  // kHot's mass is the hot mass it accumulates anyway, kFull / kTail
+  // accumulate it relative to the first batch's maximum (nuc_mass)
+  const bool nuc = nucleus_row(k, n);
+  const int32_t ke = effective_k(k, n);
+  const bool nuc_mass = nuc && MODE != kHot;
   // kHot excludes penalized ids from the stream (bitmap) so it needs no widening
-  const uint32_t kp = (uint32_t)min64(n, (int64_t)k + (MODE == kHot ? 0 : plen));
+  const uint32_t kp = (uint32_t)min64(n, (int64_t)ke + (MODE == kHot ? 0 : plen));
   if (route_row(a, MODE, k, plen, n) != kRouteTopk) continue;   // another kernel's row (cluster-uniform)
 
   const T* rowp = domain_row<T>(a, row, MODE);
@@ -182,7 +190,19 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
   // exact near the top), pairwise f32 sums per vector, one f64 add per vector
   auto hot_exp = [&](float x) -> float { return ex2_fast(((x - mtau_hi) - mtau_lo) * s2); };
   auto accum = [&](float x, int64_t pos) {
-    if (MODE == kHot && !pen_bit(pos)) sh += (double)hot_exp(x);
+    if ((MODE == kHot && !pen_bit(pos)) || nuc_mass) sh += (double)hot_exp(x);
+  };
+  // nucleus mass of kFull / kTail: every element (penalized ones are swapped
+  // for their exact terms in the final stage)
+  auto accum_vec_all = [&](const uint4& vv) {
+    float e[EPV];
+#pragma unroll
+    for (int i = 0; i < EPV; ++i) e[i] = hot_exp(vec_elem<T>(vv, i));
+#pragma unroll
+    for (int st = 1; st < EPV; st <<= 1)
+#pragma unroll
+      for (int i = 0; i < EPV; i += 2 * st) e[i] += e[i + st];
+    sh += (double)e[0];
   };
   auto accum_vec = [&](const uint4& vv, int32_t idx) {
     const uint32_t p0 = (uint32_t)(a0 + idx * EPV);
@@ -281,11 +301,20 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
       const uint32_t sorted = warp_sort_desc(f32_key(mx));
       const uint32_t t_lbk = __shfl_sync(0xffffffffu, sorted, kw <= 32 ? kw - 1 : 31);
       const uint32_t t_ek = __shfl_sync(0xffffffffu, sorted, rw - 1);
+      const float mx_w = warp_max(mx);
       if (lane == 0) {
         ms.thr_warp[warp] = kw <= 32 ? key_f32(t_lbk) : -INFINITY;
         ms.est_warp[warp] = key_f32(t_ek);
+        ms.max_warp[warp] = mx_w;
       }
       __syncthreads();
+      if (nuc_mass) {   // mass reference: the maximum of this CTA's first batch
+        float c = ms.max_warp[0];
+#pragma unroll
+        for (int w = 1; w < NW; ++w) c = fmaxf(c, ms.max_warp[w]);
+        mtau_hi = c;
+        mtau_lo = 0.f;
+      }
       float tl = ms.thr_warp[0];
       float ev[NW];
 #pragma unroll
@@ -312,6 +341,7 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
       for (int j = 0; j < U; ++j) {
         const int32_t idx = base + j * 32 + (int32_t)lane;
         if (MODE == kHot && pass_no == 0 && idx < v_hi) accum_vec(v[j], idx);
+        else if (nuc_mass && pass_no == 0 && idx < v_hi) accum_vec_all(v[j]);
         bool any = false;
 #pragma unroll
         for (int e = 0; e < EPV; ++e) any |= vec_elem<T>(v[j], e) >= thr_f;
@@ -385,13 +415,13 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
       if (get_c(i, kk) && kk >= t) sel[atomicAdd(&ms.nsel, 1u)] = kk;
     }
   }
-  if (MODE == kHot) {
+  if (MODE == kHot || nuc_mass) {
     const double s = warp_sum(sh);
     if (lane == 0) ms.sh_warp[warp] = s;
   }
   __syncthreads();
   double sh_cta = 0.0;
-  if (MODE == kHot) {
+  if (MODE == kHot || nuc_mass) {
     for (int w = 0; w < NW; ++w) sh_cta += ms.sh_warp[w];   // fixed order: deterministic
   }
   const uint32_t nsel_own = ms.nsel;
@@ -404,7 +434,8 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
       for (uint32_t i = tid; i < nsel_own; i += NT) st_dsmem_u64(dst + 8u * i, sel[i]);
       if (tid == 0) {
         st_dsmem_u32(dsmem_addr(&ms.recv_n[rank], 0), nsel_own);
-        if (MODE == kHot) st_dsmem_f64(dsmem_addr(&ms.sh_recv[rank], 0), sh_cta);
+        if (MODE == kHot || nuc_mass) st_dsmem_f64(dsmem_addr(&ms.sh_recv[rank], 0), sh_cta);
+        if (nuc_mass) st_dsmem_f32(dsmem_addr(&ms.c_recv[rank], 0), mtau_hi);
       }
       __syncthreads();
       if (tid == 0) mbar_remote_arrive(dsmem_addr(&ms.mbar, 0));
@@ -424,6 +455,8 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
       for (uint32_t i = tid; i < nr; i += NT) mrg[off + i] = src[i];
       off += nr;
       if (MODE == kHot) sh_cta += ms.sh_recv[r];
+      // nucleus mass of rank r is relative to its own reference: rescale
+      if (nuc_mass) sh_cta += ms.sh_recv[r] * exp(((double)ms.c_recv[r] - (double)mtau_hi) / p.temperature);
     }
     __syncthreads();
     if (tid == 0) ms.nsel = 0u;
@@ -440,7 +473,7 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
   {
     const FinLayout F = fin_layout(a.lcap);
     finish_row<T, MODE, NT>(a, row, p, plen, rowp, lo, n, sel, ms.nsel, sh_cta, mrow, smem + L.cand, F, ms.fin, tid,
-                            [] { __syncthreads(); });
+                            [] { __syncthreads(); }, nullptr, mtau_hi);
   }
   if (split > 1) {
     cluster_sync();   // end of row: the receive buffers may be rewritten

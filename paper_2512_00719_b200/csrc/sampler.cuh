@@ -36,6 +36,9 @@ struct SampleArgs {
   int32_t use_warp;             // this call runs the warp-per-row kernel (sample_warp.cu)
   const void* tail_logits;      // split SHVS storage: positions [H, V) of row b at
   int64_t tail_ld;              //   tail_logits + b * tail_ld (device or mapped host memory)
+  int32_t* fb_rows;             // nucleus rows whose kept set left the candidate list:
+  int32_t* fb_count;            //   appended here for the general kernel (NULL: none routed)
+  int32_t force_general;        // the general kernel decides every listed row
 };
 
 DP_DEV int64_t dom_lo(const SampleArgs& a, int mode) { return mode == kTail ? a.H : 0; }
@@ -81,6 +84,16 @@ DP_DEV int32_t pen_len(const SampleArgs& a, int row, const dp_params_t& p) {
 //  * per-row CTA / cluster streaming top-k kernel (sample_topk.cu);
 //  * general radix kernel (no top-k / oversized lists, sample_general.cu).
 enum Route : int { kRouteGeneral = 0, kRouteTopk = 1, kRouteWarp = 2 };
+// Rows with top-k off (top-p only, min-p only, neutral) take the top-k kernel
+// as "nucleus" rows: it keeps the exact kNucK largest ready values plus the
+// mass of the whole domain, and decides the row when the kept set (and the
+// draw) lies inside that list — the usual case for LLM distributions.
+// Otherwise the row goes to the general kernel (fb_rows).
+constexpr int kNucK = 512;
+DP_DEV bool nucleus_row(int32_t k, int64_t n) { return k <= 0 || (int64_t)k >= n; }
+DP_DEV int32_t effective_k(int32_t k, int64_t n) {
+  return nucleus_row(k, n) ? (int32_t)min64(n, (int64_t)kNucK) : k;
+}
 constexpr int kWarpKMax = 64;     // top_k limit of the warp kernel
 constexpr int kWarpKpMax = 256;   // raw candidates kept (k + penalty list)
 constexpr int kWarpPenCap = 256;  // penalty-list capacity it can hash
@@ -90,7 +103,12 @@ DP_DEV bool warp_row_ok(const SampleArgs& a, int32_t k, int32_t plen, int64_t n)
          a.pen.cap <= kWarpPenCap;
 }
 DP_DEV int route_row(const SampleArgs& a, int mode, int32_t k, int32_t plen, int64_t n) {
+  if (a.force_general) return kRouteGeneral;
   if (a.use_warp && warp_row_ok(a, k, plen, n)) return kRouteWarp;
+  if (nucleus_row(k, n)) {
+    if (!a.fb_rows || (int64_t)kNucK * 2 > n) return kRouteGeneral;   // no fallback list / short domain
+    k = kNucK;
+  }
   const uint32_t kp = (uint32_t)min64(n, (int64_t)k + (mode == kHot ? 0 : plen));
   if (k > 0 && (int64_t)k < n && kp <= (uint32_t)a.kcap && (uint32_t)(k + 2 * plen) <= (uint32_t)a.lcap)
     return kRouteTopk;
@@ -238,6 +256,79 @@ DP_DEV DrawResult warp_filter_draw_reg(const double* r, int32_t k, const dp_para
   res.index = js;
   res.kept = kept;
   res.logprob = log(w_at(js) / S);
+  res.margin = fmin(margin, dm / S);
+  return res;
+}
+
+// Nucleus rows (top-k off): r[0..K) are the K largest ready values of the
+// domain (sorted), `total` the mass of the WHOLE domain relative to r[0].
+// Same law as warp_filter_draw over the full domain (filtering.py:61-162);
+// exact whenever the kept set — and for neutral rows the draw — lies inside
+// the list.  `fallback` is set otherwise (the general kernel decides).
+DP_DEV DrawResult warp_filter_draw_nuc(const double* r, int32_t K, const dp_params_t& p, double u, double total,
+                                       double* w, double* cum, bool& fallback) {
+  const uint32_t lane = lane_id();
+  const double r0 = r[0];
+  double carry = 0.0;
+  for (int32_t base = 0; base < K; base += 32) {
+    const int32_t j = base + lane;
+    const double wj = j < K ? exp(r[j] - r0) : 0.0;
+    const double c = warp_incl_scan(wj) + carry;
+    if (j < K) {
+      w[j] = wj;
+      cum[j] = c;
+    }
+    carry = __shfl_sync(0xffffffffu, c, 31);
+  }
+  __syncwarp();
+  fallback = false;
+  int32_t kept = K;
+  double margin = 1e300;
+  const bool neutral = !(p.top_p < 1.0) && !(p.min_p > 0.0);
+  bool p_open = false, m_open = false;
+  if (p.top_p < 1.0) {                               // filtering.py:91-95 over the whole domain
+    const double thr = p.top_p * total;
+    int32_t below = 0;
+    for (int32_t base = 0; base < K; base += 32) {
+      const int32_t j = base + lane;
+      below += __popc(__ballot_sync(0xffffffffu, j < K && cum[j] < thr));
+    }
+    p_open = below >= K;                             // the nucleus may extend past the list
+    const int32_t kp = below + 1;
+    kept = min(kept, kp);
+    for (int32_t j = max(0, kp - 2); j < min(K, kp + 1); ++j) margin = fmin(margin, fabs(cum[j] - thr));
+    margin /= total;
+  }
+  if (p.min_p > 0.0) {                               // filtering.py:96-98
+    const double floor_ = p.min_p;                   // w_0 = 1
+    int32_t ge = 0;
+    for (int32_t base = 0; base < K; base += 32) {
+      const int32_t j = base + lane;
+      ge += __popc(__ballot_sync(0xffffffffu, j < K && w[j] >= floor_));
+    }
+    m_open = ge >= K;                                // more kept ids may follow the list
+    kept = min(kept, ge);
+    for (int32_t j = max(0, ge - 1); j < min(K, ge + 1); ++j) margin = fmin(margin, fabs(w[j] - floor_));
+  }
+  // the kept count is known once either active filter closes inside the list
+  // (kept = min of the two); both open -> the general kernel decides
+  if (!neutral && (p.top_p < 1.0 ? p_open : true) && (p.min_p > 0.0 ? m_open : true)) fallback = true;
+  kept = max(1, kept);
+  const double S = neutral ? total : cum[kept - 1];
+  const double us = u * S;
+  int32_t le = 0;
+  for (int32_t base = 0; base < kept; base += 32) {
+    const int32_t j = base + lane;
+    le += __popc(__ballot_sync(0xffffffffu, j < kept && cum[j] <= us));
+  }
+  if (neutral && le >= kept) fallback = true;        // the draw lands past the list
+  const int32_t js = min(le, kept - 1);
+  double dm = fabs(cum[js] - us);
+  if (js > 0) dm = fmin(dm, fabs(cum[js - 1] - us));
+  DrawResult res;
+  res.index = js;
+  res.kept = kept;
+  res.logprob = log(w[js] / S);
   res.margin = fmin(margin, dm / S);
   return res;
 }
