@@ -231,7 +231,7 @@ DP_DEV void warp_sort_regs(uint64_t* fkey, uint32_t* fpos) {
 // sel[0..nsel): unique (value desc, position asc) keys of the raw candidates.
 // `pp` holds the prefetched first 2*NT penalty entries.
 // Returns false when a kHot row was rejected (token left to the tail pass).
-template <typename T, int MODE, int NT, typename Sync>
+template <typename T, int MODE, int NT, bool NUC, typename Sync>
 DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32_t plen, const T* rowp,
                        int64_t lo, int64_t n, const uint64_t* sel, uint32_t nsel, double sh_unpen, double mrow,
                        uint8_t* fin, const FinLayout& F, FinishScratch& fs, uint32_t t, Sync sync,
@@ -240,8 +240,8 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
   // nucleus rows (top-k off): the list holds the kNucK largest; sh_unpen is
   // the domain mass (kHot: hot mass relative to mrow; kFull / kTail: every
   // element's f32 term relative to cref, penalized ones swapped below)
-  const bool nuc = nucleus_row(p.top_k, n);
-  const int32_t k = effective_k(p.top_k, n);
+  const bool nuc = NUC && nucleus_row(p.top_k, n);
+  const int32_t k = nuc ? effective_k(p.top_k, n) : p.top_k;
   const int32_t* pids = a.pen.ids + (int64_t)row * a.pen.cap;
   const int32_t* pcnt = a.pen.out_count + (int64_t)row * a.pen.cap;
   uint64_t* fkey = reinterpret_cast<uint64_t*>(fin + F.key);

@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_sample_kernel(Sample
       const uint32_t nsel = tmp;
       long long c2 = clock64();
       const FinLayout F = fin_layout(a.lcap);
-      finish_row<T, MODE, kNF>(a, row, p, R.plen, rowp, lo, n, sel, nsel, R.sh,
+      finish_row<T, MODE, kNF, false>(a, row, p, R.plen, rowp, lo, n, sel, nsel, R.sh,
                                MODE == kHot ? a.row_max[row] : 0.0, fin, F, ms.fin[g], t, fsync, &pp);
       if (a.dbg.stats && t == 0) {
         long long c3 = clock64();

@@ -83,7 +83,9 @@ __host__ __device__ inline TopkLayout topk_layout(int ccap, int kcap, int lcap, 
 }
 
 
-template <typename T, int MODE, int NT, int U>
+// NUC: the call may hold nucleus rows (top-k off); the plain top-k
+// instantiation carries none of that code
+template <typename T, int MODE, int NT, int U, bool NUC>
 __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample_kernel(SampleArgs a) {
   constexpr int NW = NT / 32;
   constexpr int EPV = Elem<T>::kPerVec;
@@ -118,8 +120,8 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
   // nucleus rows (top-k off) keep the kNucK largest plus the domain mass;
   // kHot's mass is the hot mass it accumulates anyway, kFull / kTail
   // accumulate it relative to the first batch's maximum (nuc_mass)
-  const bool nuc = nucleus_row(k, n);
-  const int32_t ke = effective_k(k, n);
+  const bool nuc = NUC && nucleus_row(k, n);
+  const int32_t ke = nuc ? effective_k(k, n) : k;
   const bool nuc_mass = nuc && MODE != kHot;
   // kHot excludes penalized ids from the stream (bitmap) so it needs no widening
   const uint32_t kp = (uint32_t)min64(n, (int64_t)ke + (MODE == kHot ? 0 : plen));
@@ -472,8 +474,8 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
   // ---- final stage (CTA 0): penalties, exact sort, filter, draw
   {
     const FinLayout F = fin_layout(a.lcap);
-    finish_row<T, MODE, NT>(a, row, p, plen, rowp, lo, n, sel, ms.nsel, sh_cta, mrow, smem + L.cand, F, ms.fin, tid,
-                            [] { __syncthreads(); }, nullptr, mtau_hi);
+    finish_row<T, MODE, NT, NUC>(a, row, p, plen, rowp, lo, n, sel, ms.nsel, sh_cta, mrow, smem + L.cand, F, ms.fin,
+                                 tid, [] { __syncthreads(); }, nullptr, mtau_hi);
   }
   if (split > 1) {
     cluster_sync();   // end of row: the receive buffers may be rewritten
@@ -487,13 +489,13 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
 // ---------------------------------------------------------------------------
 // host launcher
 
-template <typename T, int MODE, int NT>
+template <typename T, int MODE, bool NUC>
 static cudaError_t launch_topk_t(const SampleArgs& a, int grid_rows, cudaStream_t st) {
-  constexpr int U = 8;
+  constexpr int U = 8, NT = 256;
   const int64_t n = MODE == kFull ? a.V : (MODE == kHot ? a.H : a.V - a.H);
   const int bm_words = MODE == kHot ? (int)((n + 31) / 32) + 1 : 0;
   const TopkLayout L = topk_layout<NT>(a.wcap, a.kcap, a.lcap, bm_words, a.split);
-  auto kern = topk_sample_kernel<T, MODE, NT, U>;
+  auto kern = topk_sample_kernel<T, MODE, NT, U, NUC>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
@@ -511,21 +513,21 @@ static cudaError_t launch_topk_t(const SampleArgs& a, int grid_rows, cudaStream_
   return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
-template <int NT>
-static cudaError_t launch_topk_nt(const SampleArgs& a, int dtype, int mode, int grid_rows, cudaStream_t st) {
-  if (dtype == DP_F32) {
-    if (mode == kFull) return launch_topk_t<float, kFull, NT>(a, grid_rows, st);
-    if (mode == kHot) return launch_topk_t<float, kHot, NT>(a, grid_rows, st);
-    return launch_topk_t<float, kTail, NT>(a, grid_rows, st);
-  }
-  if (mode == kFull) return launch_topk_t<__nv_bfloat16, kFull, NT>(a, grid_rows, st);
-  if (mode == kHot) return launch_topk_t<__nv_bfloat16, kHot, NT>(a, grid_rows, st);
-  return launch_topk_t<__nv_bfloat16, kTail, NT>(a, grid_rows, st);
+template <typename T, bool NUC>
+static cudaError_t launch_topk_m(const SampleArgs& a, int mode, int grid_rows, cudaStream_t st) {
+  if (mode == kFull) return launch_topk_t<T, kFull, NUC>(a, grid_rows, st);
+  if (mode == kHot) return launch_topk_t<T, kHot, NUC>(a, grid_rows, st);
+  return launch_topk_t<T, kTail, NUC>(a, grid_rows, st);
 }
 
+// 256 threads per CTA (the 128-thread variant measured slower at every
+// shape); the nucleus instantiation only when the call may hold such rows
 cudaError_t launch_topk(const SampleArgs& a, int dtype, int mode, int grid_rows, cudaStream_t st) {
-  return a.nt == 128 ? launch_topk_nt<128>(a, dtype, mode, grid_rows, st)
-                     : launch_topk_nt<256>(a, dtype, mode, grid_rows, st);
+  const bool nuc = a.fb_rows != nullptr;
+  if (dtype == DP_F32)
+    return nuc ? launch_topk_m<float, true>(a, mode, grid_rows, st) : launch_topk_m<float, false>(a, mode, grid_rows, st);
+  return nuc ? launch_topk_m<__nv_bfloat16, true>(a, mode, grid_rows, st)
+             : launch_topk_m<__nv_bfloat16, false>(a, mode, grid_rows, st);
 }
 
 }  // namespace dp
