@@ -336,26 +336,41 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
       thr = te == -INFINITY ? 0ull : ((uint64_t)f32_key(te) << 32);
     }
     if (rank == 0 && warp == 0) head_tail(pass_no == 0);
-    // consume batches
+    // consume batches.  While the threshold is a plain value (low key bits
+    // zero) "x >= thr_f" IS the exact admission test: one max + compare per
+    // vector.  After an overflow cut it is a full composite key and the exact
+    // (value, position) test runs (ties at its value must not re-admit, so
+    // every re-stream admits strictly fewer elements).
+    const bool exact_mode = (uint32_t)thr != 0u;
     while (true) {
       uint32_t vm = 0;
+      const bool full = base + 32 * U <= v_hi;   // warp-uniform: every vector of the batch is valid
 #pragma unroll
       for (int j = 0; j < U; ++j) {
         const int32_t idx = base + j * 32 + (int32_t)lane;
-        if (MODE == kHot && pass_no == 0 && idx < v_hi) accum_vec(v[j], idx);
-        else if (nuc_mass && pass_no == 0 && idx < v_hi) accum_vec_all(v[j]);
-        bool any = false;
+        if (MODE == kHot && pass_no == 0 && (full || idx < v_hi)) accum_vec(v[j], idx);
+        else if (nuc_mass && pass_no == 0 && (full || idx < v_hi)) accum_vec_all(v[j]);
+        float mx = vec_elem<T>(v[j], 0);
 #pragma unroll
-        for (int e = 0; e < EPV; ++e) any |= vec_elem<T>(v[j], e) >= thr_f;
-        if (any && idx < v_hi) {
-          // exact (value, position) test: after an overflow cut the threshold
-          // is a full composite key, and ties at its value must not re-admit
-          // (guarantees every re-stream admits strictly fewer elements)
-          bool ex = false;
+        for (int e = 1; e < EPV; ++e) mx = fmaxf(mx, vec_elem<T>(v[j], e));
+        vm |= (mx >= thr_f ? 1u : 0u) << j;
+      }
+      if (!full) {
 #pragma unroll
-          for (int e = 0; e < EPV; ++e)
-            ex |= comp_key(vec_elem<T>(v[j], e), (uint32_t)(a0 + idx * EPV + e)) >= thr;
-          if (ex) vm |= 1u << j;
+        for (int j = 0; j < U; ++j)
+          if (base + j * 32 + (int32_t)lane >= v_hi) vm &= ~(1u << j);
+      }
+      if (exact_mode && vm) {
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+          if ((vm >> j) & 1u) {
+            const int32_t idx = base + j * 32 + (int32_t)lane;
+            bool ex = false;
+#pragma unroll
+            for (int e = 0; e < EPV; ++e)
+              ex |= comp_key(vec_elem<T>(v[j], e), (uint32_t)(a0 + idx * EPV + e)) >= thr;
+            if (!ex) vm &= ~(1u << j);
+          }
         }
       }
       if (vm) {
@@ -375,10 +390,16 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
       }
       base += NT * U;
       if (base >= v_hi) break;
+      if (base + 32 * U <= v_hi) {   // full batch: unpredicated loads at immediate offsets
+        const uint4* q = vp + base + (int32_t)lane;
 #pragma unroll
-      for (int j = 0; j < U; ++j) {
-        const int32_t idx = base + j * 32 + (int32_t)lane;
-        v[j] = idx < v_hi ? ld_stream16(vp + idx) : neg_inf_vec<T>();
+        for (int j = 0; j < U; ++j) v[j] = ld_stream16(q + j * 32);
+      } else {
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+          const int32_t idx = base + j * 32 + (int32_t)lane;
+          v[j] = idx < v_hi ? ld_stream16(vp + idx) : neg_inf_vec<T>();
+        }
       }
     }
     __syncthreads();
