@@ -96,14 +96,28 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
+        if not self.samples:   # timed region shorter than the sampling period: one query right after it
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=10).stdout
+                parts = [p.strip() for p in out.strip().split(",")]
+                if len(parts) == 6:
+                    self.samples.append(parts)
+                    self.after = True
+            except Exception:
+                pass
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
         sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
         mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+        out = {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+               "reasons": reasons, "samples": len(self.samples)}
+        if getattr(self, "after", False):
+            out["note"] = "timed region shorter than the 50 ms sampling period: queried right after it"
+        return out
 
 
 # ---------------------------------------------------------------------------
@@ -579,7 +593,10 @@ def run_ours(args, cfg):
             cpu = {"value": rate, "unit": "tokens/s", "cores": cores, "kind": kind,
                    "sample": f"{nrows} rows of this workload (full-vocabulary law, same logits) looped for "
                              f"{args.cpu_seconds:.0f}s on {cores} processes ({rows} decisions), {what}"}
-        launches = {"full": 2, "shvs": 5}[variant] + 1 + (1 if world > 1 else 0)
+        # our kernels per step (ncu launch list, profiles/r1/final/launches_*.csv):
+        # full = top-k sampler + penalty update; SHVS = hot pass + tail pass +
+        # penalty update (the NCCL all-gather of N > 1 is NCCL's kernel)
+        launches = {"full": 2, "shvs": 3}[variant]
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": scaling,
