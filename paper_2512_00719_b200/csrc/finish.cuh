@@ -11,13 +11,14 @@ namespace dp {
 
 // shared-memory carve-up of the final stage
 struct FinLayout {
-  uint32_t key, r, w, cum, pos, hash, hash_cap, bytes;
+  uint32_t key, r, w, cum, pos, hash, hash_cap, bytes, cap;   // cap: entries of each list array
 };
 __host__ __device__ inline FinLayout fin_layout(int lcap) {
   FinLayout f;
   f.hash_cap = 256;   // also the radix histogram of the top-k cut
   while (f.hash_cap < 2u * (uint32_t)lcap) f.hash_cap <<= 1;
   if (lcap < 256) lcap = 256;   // the sorts pad the list to a power of two >= 128
+  f.cap = (uint32_t)lcap;
   uint32_t o = 0;
   f.key = o; o += lcap * 8u;
   f.r = o; o += lcap * 8u;
@@ -31,7 +32,9 @@ __host__ __device__ inline FinLayout fin_layout(int lcap) {
 
 struct FinishScratch {
   uint32_t nl;
-  uint32_t pad;
+  uint32_t np;       // penalized entries of the domain (rank-merge path)
+  uint32_t nq;       // ... that can enter the top-k
+  uint32_t wc[32];   // per-warp counts of a block scan
   double sh_pen[32];
   double corr[32];
 };
@@ -344,13 +347,20 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
 
   // penalized positions of this domain -> hash set (raw candidates defer to them)
   // (kHot streamed around them already: no hash set needed)
-  if (t == 0) fs.nl = 0u;
+  if (t == 0) {
+    fs.nl = 0u;
+    fs.np = 0u;
+    fs.nq = 0u;
+  }
   if (MODE != kHot)
     for (uint32_t i = t; i < hcap; i += NT) hash[i] = 0xFFFFFFFFu;
   sync();
   const bool nuc_mass = nuc && MODE != kHot;
   const float s2 = (float)(1.4426950408889634 / p.temperature);
   const double cref_r = (double)cref / p.temperature;   // cref in ready units
+  // the rank-merge path keeps the penalized entries apart: ready values in
+  // fcum, positions at the top of fpos (k + 2 |list| < lcap: no overlap)
+  const bool fast = nsel <= 1024u;
   double m_sub = 0.0, m_add = 0.0;
   for (int32_t j = t; j < plen; j += NT) {
     int32_t pos, c;
@@ -362,9 +372,15 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
         while (atomicCAS(&hash[h], 0xFFFFFFFFu, (uint32_t)pos) != 0xFFFFFFFFu) h = (h + 1u) & hmask;
       }
       const double r = ready_penalized(x, c, p);
-      const uint32_t s = atomicAdd(&fs.nl, 1u);
-      fkey[s] = f64_key(r);
-      fpos[s] = (uint32_t)pos;
+      if (fast) {
+        const uint32_t s = atomicAdd(&fs.np, 1u);
+        fcum[s] = r;
+        fpos[F.cap - 1u - s] = (uint32_t)pos;
+      } else {
+        const uint32_t s = atomicAdd(&fs.nl, 1u);
+        fkey[s] = f64_key(r);
+        fpos[s] = (uint32_t)pos;
+      }
       if (nuc_mass) {   // swap the streamed f32 term (bit-identical) for the exact one
         m_sub += (double)ex2_fast(((x - cref) - 0.f) * s2);
         m_add += exp(r - cref_r);
@@ -384,71 +400,149 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
     for (int w = 0; w < NT / 32; ++w) s_dom += fs.corr[w] - fs.sh_pen[w];   // fixed order
   }
   lap(12);
-  for (uint32_t i = t; i < nsel; i += NT) {
-    const uint64_t key = sel[i];
-    const uint32_t pos = comp_pos(key);
-    bool is_pen = false;
-    if (MODE != kHot && plen > 0) {
-      uint32_t h = (pos * 2654435761u) & hmask;
-      while (true) {
-        const uint32_t hv = hash[h];
-        if (hv == pos) { is_pen = true; break; }
-        if (hv == 0xFFFFFFFFu) break;
-        h = (h + 1u) & hmask;
+  auto penalized = [&](uint32_t pos) -> bool {
+    if (MODE == kHot || plen == 0) return false;
+    uint32_t h = (pos * 2654435761u) & hmask;
+    while (true) {
+      const uint32_t hv = hash[h];
+      if (hv == pos) return true;
+      if (hv == 0xFFFFFFFFu) return false;
+      h = (h + 1u) & hmask;
+    }
+  };
+  uint32_t nl;
+  if (fast) {
+    // (1) rank sort of the raw candidates (unique composite keys): O(nsel^2 / NT)
+    for (uint32_t i = t; i < nsel; i += NT) {
+      const uint64_t key = sel[i];
+      uint32_t rank = 0;
+      for (uint32_t j = 0; j < nsel; ++j) rank += sel[j] > key ? 1u : 0u;
+      fkey[rank] = key;
+    }
+    sync();
+    // (2) the k largest unpenalized, in order: their ready values keep the raw
+    // order (x / tau is monotone), so a prefix count over the sorted keys ranks
+    // them; list U -> (fw, fpos)[0 .. nu)
+    uint32_t base_u = 0;
+    for (uint32_t c0 = 0; c0 < nsel; c0 += NT) {
+      const uint32_t i = c0 + t;
+      const uint64_t key = i < nsel ? fkey[i] : 0ull;
+      const uint32_t pos = comp_pos(key);
+      const bool unpen = i < nsel && !penalized(pos);
+      const uint32_t bal = __ballot_sync(0xffffffffu, unpen);
+      if (lane == 0) fs.wc[warp] = __popc(bal);
+      sync();
+      uint32_t before = base_u, total = 0;
+      for (int w = 0; w < NT / 32; ++w) {
+        if (w < (int)warp) before += fs.wc[w];
+        total += fs.wc[w];
+      }
+      before += __popc(bal & lanemask_lt());
+      if (unpen && before < (uint32_t)k) {
+        fw[before] = ready_plain(comp_val(key), p);
+        fpos[before] = pos;
+      }
+      base_u += total;
+      sync();
+    }
+    const uint32_t nu = min(base_u, (uint32_t)k);
+    const uint32_t np = fs.np;
+    // (3) a penalized id can enter the ready top-k only if it reaches the k-th
+    // unpenalized (ties kept: the merge orders them)
+    const bool full_k = base_u >= (uint32_t)k;
+    const double rk = full_k ? fw[k - 1] : -INFINITY;
+    // (4) rank merge of U and the qualifying penalized entries P into
+    // (fr, hash)[0 .. m), m = min(k, nu + |P|); order (ready desc, pos asc)
+    auto before_ = [](double ra, uint32_t pa, double rb, uint32_t pb) -> bool {
+      return ra > rb || (ra == rb && pa < pb);
+    };
+    for (uint32_t i = t; i < nu; i += NT) {
+      const double r = fw[i];
+      const uint32_t pos = fpos[i];
+      uint32_t f = i;
+      for (uint32_t j = 0; j < np; ++j)
+        if (fcum[j] >= rk && before_(fcum[j], fpos[F.cap - 1u - j], r, pos)) ++f;
+      if (f < (uint32_t)k) {
+        fr[f] = r;
+        hash[f] = pos;
       }
     }
-    if (!is_pen) {
-      const uint32_t s = atomicAdd(&fs.nl, 1u);
-      fkey[s] = f64_key(ready_plain(comp_val(key), p));
-      fpos[s] = pos;
+    for (uint32_t j = t; j < np; j += NT) {
+      const double r = fcum[j];
+      if (!(r >= rk)) continue;
+      atomicAdd(&fs.nq, 1u);
+      const uint32_t pos = fpos[F.cap - 1u - j];
+      uint32_t f = 0;
+      for (uint32_t q = 0; q < np; ++q)
+        if (fcum[q] >= rk && before_(fcum[q], fpos[F.cap - 1u - q], r, pos)) ++f;
+      for (uint32_t q = 0; q < nu; ++q)
+        if (before_(fw[q], fpos[q], r, pos)) ++f;
+      if (f < (uint32_t)k) {
+        fr[f] = r;
+        hash[f] = pos;
+      }
     }
-  }
-  sync();
-  const uint32_t nl = fs.nl;
-  uint32_t p2 = 128;
-  while (p2 < nl) p2 <<= 1;
-  for (uint32_t i = nl + t; i < p2; i += NT) {
-    fkey[i] = 0ull;
-    fpos[i] = 0xFFFFFFFFu;
-  }
-  sync();
-  lap(13);
-  // canonical order (ready desc, position asc): one warp through registers
-  // for short lists, all NT threads in shared memory otherwise
-  if (p2 <= 256) {
-    if (warp == 0) {
-      warp_topk_sort(fkey, fpos, nl, (uint32_t)k, hash);
-      const uint32_t m = min((uint32_t)k, nl);
-      for (uint32_t i = lane; i < m; i += 32) {
+    sync();
+    nl = min((uint32_t)k, nu + fs.nq);
+    for (uint32_t i = t; i < nl; i += NT) fpos[i] = hash[i];
+    sync();
+  } else {
+    for (uint32_t i = t; i < nsel; i += NT) {
+      const uint64_t key = sel[i];
+      const uint32_t pos = comp_pos(key);
+      if (!penalized(pos)) {
+        const uint32_t s = atomicAdd(&fs.nl, 1u);
+        fkey[s] = f64_key(ready_plain(comp_val(key), p));
+        fpos[s] = pos;
+      }
+    }
+    sync();
+    nl = fs.nl;
+    uint32_t p2 = 128;
+    while (p2 < nl) p2 <<= 1;
+    for (uint32_t i = nl + t; i < p2; i += NT) {
+      fkey[i] = 0ull;
+      fpos[i] = 0xFFFFFFFFu;
+    }
+    sync();
+    lap(13);
+    // canonical order (ready desc, position asc): one warp through registers
+    // for short lists, all NT threads in shared memory otherwise
+    if (p2 <= 256) {
+      if (warp == 0) {
+        warp_topk_sort(fkey, fpos, nl, (uint32_t)k, hash);
+        const uint32_t m = min((uint32_t)k, nl);
+        for (uint32_t i = lane; i < m; i += 32) {
+          const uint64_t kk = fkey[i];
+          const uint64_t bb = (kk >> 63) ? (kk & 0x7FFFFFFFFFFFFFFFull) : ~kk;
+          fr[i] = __longlong_as_double((long long)bb);
+        }
+        __syncwarp();
+      }
+    } else {
+      for (uint32_t size = 2; size <= p2; size <<= 1)
+        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+          for (uint32_t i = t; i < p2 / 2; i += NT) {
+            const uint32_t lo_i = 2 * stride * (i / stride) + (i % stride);
+            const uint32_t hi_i = lo_i + stride;
+            const bool desc = ((lo_i & size) == 0);
+            const uint64_t ka = fkey[lo_i], kb = fkey[hi_i];
+            const uint32_t pa = fpos[lo_i], pb = fpos[hi_i];
+            const bool a_first = ka > kb || (ka == kb && pa < pb);
+            if (a_first != desc) {
+              fkey[lo_i] = kb; fkey[hi_i] = ka;
+              fpos[lo_i] = pb; fpos[hi_i] = pa;
+            }
+          }
+          sync();
+        }
+      for (uint32_t i = t; i < nl; i += NT) {
         const uint64_t kk = fkey[i];
         const uint64_t bb = (kk >> 63) ? (kk & 0x7FFFFFFFFFFFFFFFull) : ~kk;
         fr[i] = __longlong_as_double((long long)bb);
       }
-      __syncwarp();
+      sync();
     }
-  } else {
-    for (uint32_t size = 2; size <= p2; size <<= 1)
-      for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
-        for (uint32_t i = t; i < p2 / 2; i += NT) {
-          const uint32_t lo_i = 2 * stride * (i / stride) + (i % stride);
-          const uint32_t hi_i = lo_i + stride;
-          const bool desc = ((lo_i & size) == 0);
-          const uint64_t ka = fkey[lo_i], kb = fkey[hi_i];
-          const uint32_t pa = fpos[lo_i], pb = fpos[hi_i];
-          const bool a_first = ka > kb || (ka == kb && pa < pb);
-          if (a_first != desc) {
-            fkey[lo_i] = kb; fkey[hi_i] = ka;
-            fpos[lo_i] = pb; fpos[hi_i] = pa;
-          }
-        }
-        sync();
-      }
-    for (uint32_t i = t; i < nl; i += NT) {
-      const uint64_t kk = fkey[i];
-      const uint64_t bb = (kk >> 63) ? (kk & 0x7FFFFFFFFFFFFFFFull) : ~kk;
-      fr[i] = __longlong_as_double((long long)bb);
-    }
-    sync();
   }
 
   lap(14);
@@ -463,7 +557,7 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
       if (!(total > 0.0) || !isfinite(total)) fb = true;   // e.g. the first batch missed the row's scale
       else d = warp_filter_draw_nuc(fr, (int32_t)min((uint32_t)k, nl), p, ud, total, fw, fcum, fb);
     } else {
-      d = warp_filter_draw(fr, k, p, ud, fw, fcum, a.dbg.stats);
+      d = warp_filter_draw(fr, (int32_t)min((uint32_t)k, nl), p, ud, fw, fcum, a.dbg.stats);
     }
     lap(16);
     if (fb) {

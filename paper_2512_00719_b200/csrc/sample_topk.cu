@@ -462,6 +462,9 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
       }
       __syncthreads();
       if (tid == 0) mbar_remote_arrive(dsmem_addr(&ms.mbar, 0));
+      // nothing of this CTA is read remotely: without a next row it retires
+      // now and frees its slot while CTA 0 finishes the row
+      if (ridx + (int)(gridDim.x / split) >= nrows) return;
       cluster_sync();   // end of row: CTA 0 is done with the receive buffers
       phase ^= 1u;
       continue;
@@ -499,6 +502,7 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
                                  tid, [] { __syncthreads(); }, nullptr, mtau_hi);
   }
   if (split > 1) {
+    if (ridx + (int)(gridDim.x / split) >= nrows) return;   // the peers retired after their push
     cluster_sync();   // end of row: the receive buffers may be rewritten
     phase ^= 1u;
   } else {

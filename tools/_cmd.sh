@@ -1,7 +1,7 @@
-cd "${GRAFT_REPO_ROOT:-/root/repo}"; O=gpurun_out/b3; mkdir -p $O
-bash tools/bench_all.sh b3
-timeout 900 python tools/c3_sweep.py --out $O/c3_sweep.json > $O/c3.txt 2>&1
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c2_full.csv python bench.py --steps 2 --warmup 3 --kernel-steps 2 --no-cpu-baseline --no-shvs > $O/ncu_launch.log 2>&1
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c2_shvs.csv python bench.py --variant shvs --steps 2 --warmup 3 --kernel-steps 2 --no-cpu-baseline > $O/ncu_launch2.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"topk_sample" -s 2 -c 1 -o $O/full_c2 python tools/prof_step.py --steps 4 > $O/ncu_full_c2.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"warp_sample|topk_sample" -s 2 -c 2 -o $O/full_shvs python tools/prof_step.py --variant shvs --steps 4 > $O/ncu_full_shvs.log 2>&1
+cd "${GRAFT_REPO_ROOT:-/root/repo}"; O=gpurun_out/it29; mkdir -p $O
+./tools/micro/finish > $O/finish.txt 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q > $O/pytest.txt 2>&1; echo "rc=$?" >> $O/pytest.txt
+for args in "--config c2" "--config c4" "--config c2p" "--variant shvs" "--config c1"; do
+  echo "$args" >> $O/bench.txt
+  timeout 300 python bench.py --no-cpu-baseline --no-shvs --steps 200 --warmup 3 $args 2>>$O/err.txt | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['value']), d['ms_per_step'], d['roofline']['kernel_ms'], d['roofline']['frac'])" >> $O/bench.txt 2>&1
+done

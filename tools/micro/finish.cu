@@ -20,7 +20,7 @@ __global__ void __launch_bounds__(256, MB) kern(SampleArgs a, const float* row, 
   __syncthreads();
   long long t0 = clock64();
   for (int it = 0; it < 4; ++it) {
-    finish_row<float, kTail, 256>(a, 0, p, plen, row, 0, n, sel, nsel_in, 0.0, 0.0, smem, F, fs, t,
+    finish_row<float, kTail, 256, false>(a, 0, p, plen, row, 0, n, sel, nsel_in, 0.0, 0.0, smem, F, fs, t,
                                   [] { __syncthreads(); });
     __syncthreads();
   }
