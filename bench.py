@@ -4,8 +4,9 @@ Default workload (N=1): BASELINE configs[1] — Qwen2.5 vocab V=152,064,
 B=1,024 fp32 logits, repetition/presence/frequency penalties + top-k/top-p/
 min-p, synthetic logits from the SyntheticSource formula generated on device.
 A step = one pass of the hot path over the batch: dp_sample_full (fused
-penalties -> tau -> top-k -> top-p -> min-p -> draw) + the penalty-state
-update (the reference's timed unit, harness.py:274-279).  With N GPUs each rank
+penalties -> tau -> top-k -> top-p -> min-p -> draw, with the penalty-state
+update fused into the deciding kernel) — the reference's timed unit,
+sample + update_output_histogram (harness.py:274-279).  With N GPUs each rank
 owns a fixed 1,024-row slice (weak scaling) and the step ends with the
 token-id all-gather over NCCL.
 
@@ -331,9 +332,7 @@ def measure_shvs_e2e(args, cfg, plane_kw, src, seq_ids, dev, shard, world):
         it = base_it[0] + i
         if it % RESET_EVERY == 0 and it > 0:
             plane.state.reset()
-        d = plane.sample(bufs[it & 1], it, variant="shvs", summary=summ[it & 1], summary_raw=True, update=False)
-        plane.state.update(d.token, d.flags)
-        return d
+        return plane.sample(bufs[it & 1], it, variant="shvs", summary=summ[it & 1], summary_raw=True)
 
     for i in range(args.warmup):
         step(i - args.warmup)
@@ -457,11 +456,14 @@ def run_ours(args, cfg):
         return plane.sample(bufs[it & 1], it, update=False)
 
     def step(i):
+        # sample + penalty update (fused into the deciding kernel: fuse_update)
         it = base_it[0] + i
         if it % RESET_EVERY == 0 and it > 0:
             plane.state.reset()
-        d = sample_only(i)
-        plane.state.update(d.token, d.flags)
+        if variant == "shvs":
+            d = plane.sample(bufs[it & 1], it, variant="shvs", summary=summaries[it & 1], summary_raw=True)
+        else:
+            d = plane.sample(bufs[it & 1], it)
         if world > 1:
             # token-id all-gather on a side stream: it overlaps the next step's
             # sampling (the penalty update needs only the local tokens)
@@ -594,9 +596,9 @@ def run_ours(args, cfg):
                    "sample": f"{nrows} rows of this workload (full-vocabulary law, same logits) looped for "
                              f"{args.cpu_seconds:.0f}s on {cores} processes ({rows} decisions), {what}"}
         # our kernels per step (ncu launch list, profiles/r1/final/launches_*.csv):
-        # full = top-k sampler + penalty update; SHVS = hot pass + tail pass +
-        # penalty update (the NCCL all-gather of N > 1 is NCCL's kernel)
-        launches = {"full": 2, "shvs": 3}[variant]
+        # full = the top-k sampler (penalty update fused); SHVS = hot pass +
+        # tail pass (the NCCL all-gather of N > 1 is NCCL's kernel)
+        launches = {"full": 1, "shvs": 2}[variant]
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": scaling,

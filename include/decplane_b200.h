@@ -104,7 +104,10 @@ typedef struct {
  * split: CTAs per row cluster for the streaming kernels (0 = auto, <= 8;
  *   -1 = the persistent warp-specialised TMA-ring kernel).
  * kernel: 0 = auto, 1 = per-row CTA / cluster kernel, 2 = warp-per-row kernel
- *   for rows with top_k <= 64 (auto picks it for the SHVS hot pass at B >= SMs). */
+ *   for rows with top_k <= 64 (auto picks it for the SHVS hot pass at B >= SMs).
+ * Rows with top-k off (top-p only, min-p only, neutral) are decided by the top-k
+ *   kernel from their 512 largest values plus the domain mass when min_top_k == 0,
+ *   with the general kernel as the exact fallback. */
 typedef struct {
   int32_t max_top_k;
   int32_t split;
@@ -113,7 +116,10 @@ typedef struct {
                            summary (dp_row_summary_raw); correct it for penalties */
   int32_t min_top_k;
   int32_t kernel;
-  int32_t reserved[2];
+  int32_t fuse_update;  /* record every decided token in the penalty state inside the
+                           deciding kernel (update_output_histogram, penalty.py:18-32),
+                           replacing a separate dp_penalty_update launch */
+  int32_t reserved;
 } dp_plan_t;
 
 /* Library / device info. dp_device_check returns DP_OK when `device` is sm_100. */

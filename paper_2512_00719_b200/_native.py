@@ -68,7 +68,7 @@ class Debug(C.Structure):
 class Plan(C.Structure):
     _fields_ = [("max_top_k", C.c_int32), ("split", C.c_int32), ("threads", C.c_int32),
                 ("summary_raw", C.c_int32), ("min_top_k", C.c_int32), ("kernel", C.c_int32),
-                ("reserved", C.c_int32 * 2)]
+                ("fuse_update", C.c_int32), ("reserved", C.c_int32)]
 
 
 assert C.sizeof(Params) == 64

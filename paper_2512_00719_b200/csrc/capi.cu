@@ -177,6 +177,7 @@ void plan_topk(dp::SampleArgs& a, const dp_plan_t* plan, int64_t B, int64_t n, i
   // threads per CTA: 256 by default; plan->reserved[0] may request 128
   a.nt = (plan && plan->threads == 128) ? 128 : 256;
   a.summary_raw = (plan && plan->summary_raw) ? 1 : 0;
+  a.update_pen = (plan && plan->fuse_update) ? 1 : 0;
   (void)elem_bytes;
 }
 

@@ -578,6 +578,7 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
       if (a.dbg.bytes_touched)
         a.dbg.bytes_touched[row] = (MODE == kTail ? a.dbg.bytes_touched[row] : 0ull) + (uint64_t)n * sizeof(T);
     }
+    if (!fb) warp_record_token(a, row, pos_to_id(a, (int64_t)fpos[d.index] + lo));   // fused K5
     if (a.dbg.topk_ids && !fb) {
       const int32_t m = min(k, a.dbg.topk_stride);
       for (int32_t j = lane; j < m; j += 32) {

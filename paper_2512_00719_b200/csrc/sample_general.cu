@@ -640,6 +640,7 @@ __global__ void __launch_bounds__(kGenNT, 1) general_sample_kernel(SampleArgs a)
     if (MODE == kHot && a.dbg.alpha) a.dbg.alpha[row] = alpha;
     if (a.dbg.bytes_touched)
       a.dbg.bytes_touched[row] = (MODE == kTail ? a.dbg.bytes_touched[row] : 0ull) + (uint64_t)n * sizeof(T);
+    thread_record_token(a, row, pos_to_id(a, gpos));   // fused K5
   }
   }
 }

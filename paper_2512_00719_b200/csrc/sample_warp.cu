@@ -577,6 +577,7 @@ __global__ void __launch_bounds__(kMW * 32, kMWBlocks) warp_sample_kernel(Sample
       if (a.dbg.bytes_touched) a.dbg.bytes_touched[row] = (uint64_t)n * sizeof(T);
       if (a.dbg.stats) atomicAdd((unsigned long long*)&a.dbg.stats[0], 1ull);
     }
+    warp_record_token(a, row, pos_to_id(a, (int64_t)fpos[d.index] + lo));   // fused K5
     if (a.dbg.topk_ids) {
       const int32_t m = min((int32_t)kk, a.dbg.topk_stride);
       for (int32_t j = lane; j < m; j += 32) {

@@ -39,6 +39,7 @@ struct SampleArgs {
   int32_t* fb_rows;             // nucleus rows whose kept set left the candidate list:
   int32_t* fb_count;            //   appended here for the general kernel (NULL: none routed)
   int32_t force_general;        // the general kernel decides every listed row
+  int32_t update_pen;           // record each decided token in the penalty state (fused K5)
 };
 
 DP_DEV int64_t dom_lo(const SampleArgs& a, int mode) { return mode == kTail ? a.H : 0; }
@@ -76,6 +77,58 @@ DP_DEV void get_uniforms(const SampleArgs& a, int row, const dp_params_t& p, dou
 // number of penalty entries that can change values for this row
 DP_DEV int32_t pen_len(const SampleArgs& a, int row, const dp_params_t& p) {
   return penalties_neutral(p) ? 0 : a.pen.len[row];
+}
+
+// ---------------------------------------------------------------------------
+// update_output_histogram (penalty.py:18-32) fused into the kernel that
+// decides the row: C_o[tok] += 1, a first-seen id is appended.  The row's list
+// is read by no other kernel of the call after its decision (SHVS tail and
+// fallback passes only see rows the first pass left undecided).
+DP_DEV void record_token_hit(const SampleArgs& a, int row, int32_t tok, int32_t hit, int32_t len) {
+  int32_t* ids = a.pen.ids + (int64_t)row * a.pen.cap;
+  int32_t* cnt = a.pen.out_count + (int64_t)row * a.pen.cap;
+  if (hit >= 0) {
+    cnt[hit] += 1;
+  } else if (len < a.pen.cap) {
+    ids[len] = tok;
+    cnt[len] = 1;
+    a.pen.len[row] = len + 1;
+  } else {
+    a.flags[row] |= DP_FLAG_PEN_OVERFLOW;
+  }
+}
+// one warp (all lanes, tok uniform)
+DP_DEV void warp_record_token(const SampleArgs& a, int row, int32_t tok) {
+  if (!a.update_pen || tok < 0) return;
+  const uint32_t lane = lane_id();
+  const int32_t* ids = a.pen.ids + (int64_t)row * a.pen.cap;
+  const int32_t len = a.pen.len[row];
+  int32_t hit = -1;
+  for (int32_t base = 0; base < len && hit < 0; base += 256) {
+    int32_t v[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int32_t j = base + r * 32 + (int32_t)lane;
+      v[r] = j < len ? ids[j] : -1;
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const uint32_t m = __ballot_sync(0xffffffffu, v[r] == tok);
+      if (m && hit < 0) hit = base + r * 32 + __ffs(m) - 1;
+    }
+  }
+  if (lane == 0) record_token_hit(a, row, tok, hit, len);
+  __syncwarp();
+}
+// one thread
+DP_DEV void thread_record_token(const SampleArgs& a, int row, int32_t tok) {
+  if (!a.update_pen || tok < 0) return;
+  const int32_t* ids = a.pen.ids + (int64_t)row * a.pen.cap;
+  const int32_t len = a.pen.len[row];
+  int32_t hit = -1;
+  for (int32_t j = 0; j < len; ++j)
+    if (ids[j] == tok) { hit = j; break; }
+  record_token_hit(a, row, tok, hit, len);
 }
 
 // ---------------------------------------------------------------------------

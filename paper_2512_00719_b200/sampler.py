@@ -172,6 +172,8 @@ class DecisionPlane:
         dbg = self._debug_struct(d, topk_stride, debug)
         st = _stream()
         uni = _ptr(uniforms)
+        # the penalty update runs inside the deciding kernels (no extra launch)
+        self._plan.fuse_update = 1 if update else 0
         if variant == VARIANT_FULL:
             N.call("dp_sample_full", _ptr(logits), dt, self.batch, self.vocab_size, logits.stride(0),
                    _ptr(self._params_dev), C.byref(self.state.native), uni, _ptr(self._seq_dev), int(iteration),
@@ -190,8 +192,6 @@ class DecisionPlane:
                    _ptr(d.logprob), _ptr(d.flags), C.byref(dbg), C.byref(self._plan), _ptr(self._scratch), st)
         else:
             raise ValueError(f"unknown variant {variant!r}")
-        if update:
-            self.state.update(d.token, d.flags)
         return d
 
     def sample_split(self, hot, tail, iteration: int, summary, uniforms=None, update: bool = True,
@@ -220,12 +220,11 @@ class DecisionPlane:
         perm, inv = self.hot.device_maps(self.device)
         rmax, tot = summary
         self._plan.summary_raw = 1 if summary_raw else 0
+        self._plan.fuse_update = 1 if update else 0
         N.call("dp_sample_shvs_split", _ptr(hot), hot.stride(0), _ptr(tail), tail.stride(0), dt, self.batch,
                self.vocab_size, h, _ptr(perm), _ptr(inv), _ptr(rmax), _ptr(tot), _ptr(self._params_dev),
                C.byref(self.state.native), _ptr(uniforms), _ptr(self._seq_dev), int(iteration), _ptr(d.token),
                _ptr(d.logprob), _ptr(d.flags), C.byref(dbg), C.byref(self._plan), _ptr(self._scratch), _stream())
-        if update:
-            self.state.update(d.token, d.flags)
         return d
 
     def sample_host(self, logits_host, iteration: int, summary_host, staging=None, update: bool = True,

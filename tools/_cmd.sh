@@ -1,7 +1,6 @@
-cd "${GRAFT_REPO_ROOT:-/root/repo}"; O=gpurun_out/it29; mkdir -p $O
-./tools/micro/finish > $O/finish.txt 2>&1
+cd "${GRAFT_REPO_ROOT:-/root/repo}"; O=gpurun_out/it30; mkdir -p $O
 timeout 900 python -m pytest tests -m gpu -x -q > $O/pytest.txt 2>&1; echo "rc=$?" >> $O/pytest.txt
-for args in "--config c2" "--config c4" "--config c2p" "--variant shvs" "--config c1"; do
+for args in "--config c2" "--config c4" "--variant shvs" "--config c5 --steps 30"; do
   echo "$args" >> $O/bench.txt
   timeout 300 python bench.py --no-cpu-baseline --no-shvs --steps 200 --warmup 3 $args 2>>$O/err.txt | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['value']), d['ms_per_step'], d['roofline']['kernel_ms'], d['roofline']['frac'])" >> $O/bench.txt 2>&1
 done
