@@ -1,0 +1,40 @@
+"""Small end-to-end workload for compute-sanitizer (memcheck / racecheck /
+synccheck): full path, SHVS (whole and split storage), nucleus rows, the
+general fallback, penalty update and reset, on a few rows.
+
+    compute-sanitizer --tool racecheck python tools/sanitize.py
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2512_00719_b200 import DecisionPlane, HotVocab, SamplingParams  # noqa: E402
+from paper_2512_00719_b200.synthetic import SyntheticSource  # noqa: E402
+
+v, b = 8192, 12
+kinds = [dict(temperature=0.8, top_k=50, top_p=0.9, min_p=0.05, rep_penalty=1.1, presence_penalty=0.5,
+              frequency_penalty=0.1), dict(temperature=0.7, top_p=0.9), dict(temperature=9.0),
+         dict(temperature=1.0, top_k=1), dict(temperature=6.0, top_p=0.99, rep_penalty=1.2)]
+params = [SamplingParams(**kinds[i % len(kinds)], seed=i) for i in range(b)]
+prompts = [np.random.default_rng(i).integers(0, v, 24) for i in range(b)]
+src = SyntheticSource(v, device="cuda")
+plane = DecisionPlane(v, params, prompts=prompts, max_generated=16)
+x = src.generate(0, range(b))
+for it in range(3):
+    plane.sample(x, it)
+plane.state.reset()
+hot = HotVocab(v, src.hot_ordering()[:2048])
+plane_s = DecisionPlane(v, params, prompts=prompts, hot=hot, max_generated=16)
+xs = hot.to_hot_first(x).contiguous()
+summ = plane_s.producer_summary(xs)
+for it in range(2):
+    plane_s.sample(xs, it, variant="shvs", summary=summ, summary_raw=True)
+    plane_s.sample_split(xs[:, :2048].contiguous(), xs[:, 2048:].contiguous(), 10 + it, summ, summary_raw=True)
+plane_k = DecisionPlane(v, params, prompts=prompts, max_generated=16, kernel=2, hot=hot)
+plane_k.sample(xs, 3, variant="shvs", summary=summ, summary_raw=True)
+torch.cuda.synchronize()
+print("sanitize workload done")
