@@ -64,6 +64,18 @@ struct PenEntry {
   uint32_t bucket;
 };
 
+// 64-bit shared-memory add as two native 32-bit atomics (sm_100 has no
+// native 64-bit shared atomic add: the compiler emits a CAS loop, which
+// serialises hard on the popular buckets).  The low word's carry-out of THIS
+// addition goes to the high word, so the 64-bit total is exact.
+DP_DEV void smem_add_u64(unsigned long long* addr, unsigned long long w) {
+  uint32_t* p = reinterpret_cast<uint32_t*>(addr);
+  const uint32_t lo = (uint32_t)w, hi = (uint32_t)(w >> 32);
+  const uint32_t old = atomicAdd(p, lo);
+  const uint32_t up = hi + ((uint32_t)(old + lo) < old ? 1u : 0u);
+  if (up) atomicAdd(p + 1, up);
+}
+
 // block reductions over kGenNT threads
 template <typename F>
 DP_DEV double blk_sum_d(double v, GenSmem& g, F sync) {
@@ -320,7 +332,7 @@ __global__ void __launch_bounds__(kGenNT, 1) general_sample_kernel(SampleArgs a)
     const uint32_t b = bucket_of(x);
     const unsigned long long w = wfix(x);
     atomicAdd(&g.cnt[b], 1u);
-    if (w) atomicAdd(&g.mass[b], w);
+    if (w) smem_add_u64(&g.mass[b], w);
     wsum += w;
     ++cnp;
     if (p.min_p > 0.0 && f32_key(x) >= minp_key) {
@@ -330,7 +342,7 @@ __global__ void __launch_bounds__(kGenNT, 1) general_sample_kernel(SampleArgs a)
   }
   for (uint32_t j = tid; j < np; j += kGenNT) {
     atomicAdd(&g.cnt[pen[j].bucket], 1u);
-    atomicAdd(&g.mass[pen[j].bucket], pen[j].wfp);
+    smem_add_u64(&g.mass[pen[j].bucket], pen[j].wfp);
     wsum += pen[j].wfp;
     if (p.min_p > 0.0 && exp(pen[j].r - rmax) >= p.min_p) {
       wminp += pen[j].wfp;
@@ -446,14 +458,14 @@ __global__ void __launch_bounds__(kGenNT, 1) general_sample_kernel(SampleArgs a)
         // descending key order: digit 2047 first
         atomicAdd(&g.digit_cnt[2047u - d], 1u);
         const unsigned long long w = wfix(x);
-        if (w) atomicAdd(&g.digit_mass[2047u - d], w);
+        if (w) smem_add_u64(&g.digit_mass[2047u - d], w);
       }
       for (uint32_t j = tid; j < np; j += kGenNT) {
         const unsigned long long k = pen[j].vkey;
         if (pen[j].bucket == (uint32_t)bsel && member(k, pen[j].bucket)) {
           const uint32_t d = (uint32_t)(k >> shift) & 2047u;
           atomicAdd(&g.digit_cnt[2047u - d], 1u);
-          atomicAdd(&g.digit_mass[2047u - d], pen[j].wfp);
+          smem_add_u64(&g.digit_mass[2047u - d], pen[j].wfp);
         }
       }
       sync();
