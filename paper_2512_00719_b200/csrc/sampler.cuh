@@ -142,7 +142,7 @@ enum Route : int { kRouteGeneral = 0, kRouteTopk = 1, kRouteWarp = 2 };
 // mass of the whole domain, and decides the row when the kept set (and the
 // draw) lies inside that list — the usual case for LLM distributions.
 // Otherwise the row goes to the general kernel (fb_rows).
-constexpr int kNucK = 512;
+constexpr int kNucK = 256;
 DP_DEV bool nucleus_row(int32_t k, int64_t n) { return k <= 0 || (int64_t)k >= n; }
 DP_DEV int32_t effective_k(int32_t k, int64_t n) {
   return nucleus_row(k, n) ? (int32_t)min64(n, (int64_t)kNucK) : k;
