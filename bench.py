@@ -633,7 +633,8 @@ def main():
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--kernel-steps", type=int, default=50)
-    ap.add_argument("--hot", type=int, default=16384)
+    ap.add_argument("--hot", type=int, default=4096,
+                    help="SHVS hot-set size (4,096: the measured optimum of tools/c3_sweep.py on this source)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--variant", default="full", choices=["full", "shvs"])

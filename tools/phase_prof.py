@@ -20,7 +20,7 @@ from paper_2512_00719_b200.synthetic import SyntheticSource  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c2")
 ap.add_argument("--variant", default="shvs")
-ap.add_argument("--hot", type=int, default=16384)
+ap.add_argument("--hot", type=int, default=4096)
 ap.add_argument("--kernel", type=int, default=0)
 ap.add_argument("--steps", type=int, default=4)
 args = ap.parse_args()

@@ -26,7 +26,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--split", type=int, default=0)
     ap.add_argument("--kernel", type=int, default=0)
-    ap.add_argument("--hot", type=int, default=16384)
+    ap.add_argument("--hot", type=int, default=4096)
     ap.add_argument("--bf16", action="store_true")
     args = ap.parse_args()
     cfg = bench.CONFIGS[args.config]
