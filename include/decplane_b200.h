@@ -111,7 +111,7 @@ typedef struct {
 typedef struct {
   int32_t max_top_k;
   int32_t split;
-  int32_t threads;      /* threads per CTA of the top-k kernel: 0/256 or 128 */
+  int32_t threads;      /* ignored (kept for ABI stability): the top-k kernel runs 256 threads */
   int32_t summary_raw;  /* dp_sample_shvs: row_max/total_expsum are the producer's raw
                            summary (dp_row_summary_raw); correct it for penalties */
   int32_t min_top_k;
