@@ -433,7 +433,6 @@ def run_ours(args, cfg):
     hot = HotVocab(v, src.hot_ordering()[: args.hot]) if variant == "shvs" else None
     plane = DecisionPlane(v, params, prompts=prompts, seq_ids=seq_ids, hot=hot, device=dev,
                           max_generated=RESET_EVERY + 8, split=args.split, kernel=args.kernel)
-    plane._plan.threads = args.threads
     tdt = torch.float32 if cfg["dtype"] == "f32" else torch.bfloat16
     perm = hot.device_maps(dev)[0] if hot is not None else None
     bufs = [src.generate(i, seq_ids, dtype=tdt, perm=perm) for i in range(2)]   # 2 x batch > L2
@@ -640,7 +639,6 @@ def main():
     ap.add_argument("--variant", default="full", choices=["full", "shvs"])
     ap.add_argument("--split", type=int, default=0)
     ap.add_argument("--kernel", type=int, default=0, help="dp_plan_t.kernel: 0 auto, 1 CTA/cluster, 2 warp-per-row")
-    ap.add_argument("--threads", type=int, default=0, help="dp_plan_t.threads of the top-k kernel (0/256 or 128)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-seconds", type=float, default=5.0)
     ap.add_argument("--ref-budget", type=float, default=90.0)

@@ -394,3 +394,36 @@ def test_nucleus_rows_match_oracle(torch_cuda, bf16):
             states[b].update(int(dec[b].token))
         plane_s.state.update(torch.from_numpy(np.array([dd.token for dd in dec], np.int32)).cuda())
     print("exemptions:", exempt)
+
+
+def test_sample_host_matches_device_path(torch_cuda):
+    """DecisionPlane.sample_host (host-resident hot-first logits: hot prefix
+    staged with dp_stage_hot, tail read zero-copy) decides exactly like the
+    device-resident SHVS call on the same rows, and records the same penalty
+    state (fused update)."""
+    torch = torch_cuda
+    from paper_2512_00719_b200 import DecisionPlane, HotVocab, SamplingParams
+    from paper_2512_00719_b200.synthetic import SyntheticSource
+
+    v, bsz, h = 32000, 64, 1024
+    kw = dict(temperature=0.8, top_k=50, top_p=0.9, min_p=0.05, rep_penalty=1.1, presence_penalty=0.5,
+              frequency_penalty=0.1)
+    prompts = [np.random.default_rng(b).integers(0, v, 32) for b in range(bsz)]
+    src = SyntheticSource(v, device="cuda")
+    hot = HotVocab(v, src.hot_ordering()[:h])
+    a = DecisionPlane(v, [SamplingParams(**kw, seed=b) for b in range(bsz)], prompts=prompts, hot=hot)
+    b = DecisionPlane(v, [SamplingParams(**kw, seed=b) for b in range(bsz)], prompts=prompts, hot=hot)
+    perm = hot.device_maps(a.device)[0]
+    for it in range(4):
+        x = src.generate(it, range(bsz), perm=perm)
+        summ = a.producer_summary(x)
+        da = a.sample(x, it, variant="shvs", summary=summ, summary_raw=True)
+        host = x.cpu().pin_memory()
+        sh = (summ[0].cpu().pin_memory(), summ[1].cpu().pin_memory())
+        db = b.sample_host(host, it, sh, summary_raw=True)
+        torch.cuda.synchronize()
+        assert torch.equal(da.token, db.token), it
+        assert torch.equal(da.flags, db.flags), it
+        assert torch.equal(da.logprob, db.logprob), it
+    for (ia, ca), (ib, cb) in zip(a.state.rows(), b.state.rows()):
+        assert np.array_equal(ia, ib) and np.array_equal(ca, cb)
