@@ -364,12 +364,12 @@ int sample_shvs_impl(const void* logits, int dtype, int64_t B, int64_t V, int64_
   if (nuc && (e = arm_fallback(t, 2, B, st)) != cudaSuccess) return cuda_status(e, "dp_sample_shvs/fallback");
   plan_topk(t, plan_host, B, V - H, dtype == DP_F32 ? 4 : 2);
   // The tail pass serves only the rejected rows (typically a few percent of
-  // B, count known on the device only): 8-CTA clusters split each row over 8
+  // B, count known on the device only): 4-CTA clusters split each row over 4
   // SMs, and the clusters loop over the reject list, so a handful of
   // rejections costs one short row time rather than one long one.
   int64_t tail_clusters = B;
   if (!persistent && !(plan_host && plan_host->split > 0)) {
-    t.split = (V - H) >= 8 * 4096 ? 8 : 1;
+    t.split = (V - H) >= 4 * 4096 ? 4 : 1;   // 4 measured best at C2 (2: 71, 4: 63, 8: 65 us per SHVS step)
     const int64_t slots = (int64_t)sm_count() * 2 / t.split;   // resident clusters (2 tail CTAs per SM)
     tail_clusters = B < slots ? B : slots;
   }

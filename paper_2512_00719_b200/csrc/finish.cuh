@@ -548,9 +548,12 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
   lap(14);
   if (warp == 0) {
     const double ud = u[MODE == kTail ? 2 : 0];
+    // no usable mass: every candidate is -inf (DegenerateRowError, core.py:19-20)
+    const bool degen = !(nl > 0 && fr[0] > -INFINITY);
     bool fb = false;
     DrawResult d;
-    if (nuc) {
+    if (degen) {
+    } else if (nuc) {
       // domain mass relative to the top ready value r[0]
       const double ref = MODE == kHot ? mrow : cref_r;
       const double total = s_dom * exp(ref - fr[0]);
@@ -560,7 +563,13 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
       d = warp_filter_draw(fr, (int32_t)min((uint32_t)k, nl), p, ud, fw, fcum, a.dbg.stats);
     }
     lap(16);
-    if (fb) {
+    if (degen) {
+      if (lane == 0) {
+        a.token[row] = -1;
+        a.logprob[row] = 0.0;
+        a.flags[row] = DP_FLAG_DEGENERATE | (MODE == kTail ? DP_FLAG_REJECTED : 0);
+      }
+    } else if (fb) {
       if (lane == 0) a.fb_rows[atomicAdd(a.fb_count, 1)] = row;   // the general kernel decides it
     } else if (lane == 0) {
       const int64_t pos = (int64_t)fpos[d.index] + lo;
@@ -578,8 +587,8 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
       if (a.dbg.bytes_touched)
         a.dbg.bytes_touched[row] = (MODE == kTail ? a.dbg.bytes_touched[row] : 0ull) + (uint64_t)n * sizeof(T);
     }
-    if (!fb) warp_record_token(a, row, pos_to_id(a, (int64_t)fpos[d.index] + lo));   // fused K5
-    if (a.dbg.topk_ids && !fb) {
+    if (!fb && !degen) warp_record_token(a, row, pos_to_id(a, (int64_t)fpos[d.index] + lo));   // fused K5
+    if (a.dbg.topk_ids && !fb && !degen) {
       const int32_t m = min(k, a.dbg.topk_stride);
       for (int32_t j = lane; j < m; j += 32) {
         a.dbg.topk_ids[(int64_t)row * a.dbg.topk_stride + j] = pos_to_id(a, (int64_t)fpos[j] + lo);

@@ -560,6 +560,14 @@ __global__ void __launch_bounds__(kMW * 32, kMWBlocks) warp_sample_kernel(Sample
       F.fr[i] = __longlong_as_double((long long)bb);
     }
     __syncwarp();
+    if (!(kk > 0 && F.fr[0] > -INFINITY)) {   // no usable mass (DegenerateRowError, core.py:19-20)
+      if (lane == 0) {
+        a.token[row] = -1;
+        a.logprob[row] = 0.0;
+        a.flags[row] = DP_FLAG_DEGENERATE;
+      }
+      continue;
+    }
     const DrawResult d = warp_filter_draw_reg(F.fr, (int32_t)kk, p, u[0]);
     lap(7);
     if (prof) atomicMax((unsigned long long*)&a.dbg.stats[22], gtime());

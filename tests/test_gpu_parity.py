@@ -427,3 +427,31 @@ def test_sample_host_matches_device_path(torch_cuda):
         assert torch.equal(da.logprob, db.logprob), it
     for (ia, ca), (ib, cb) in zip(a.state.rows(), b.state.rows()):
         assert np.array_equal(ia, ib) and np.array_equal(ca, cb)
+
+
+def test_degenerate_rows_are_flagged_and_raised(torch_cuda):
+    """A row with no usable mass (all -inf) is flagged DP_FLAG_DEGENERATE on
+    the full path, its penalty state is left alone, and to_decisions raises
+    DegenerateRowError like the reference (core.py:19-20, shvs.py:150-151) —
+    or returns None with raise_degenerate=False; the other rows decide."""
+    torch = torch_cuda
+    from paper_2512_00719_b200 import DegenerateRowError, DecisionPlane, SamplingParams
+
+    v, bsz = 4096, 4
+    kinds = [dict(temperature=0.8, top_k=50), dict(temperature=0.8, top_p=0.9), dict(temperature=1.0)]
+    for kw in kinds:
+        plane = DecisionPlane(v, [SamplingParams(**kw, seed=b) for b in range(bsz)],
+                              prompts=[[1, 2, 3]] * bsz)
+        x = torch.randn(bsz, v, device="cuda")
+        x[2] = float("-inf")
+        len_before = plane.state.len.clone()
+        d = plane.sample(x, 0)
+        torch.cuda.synchronize()
+        fl = d.flags.cpu().numpy()
+        assert fl[2] & 0x80, (kw, fl)
+        assert not (fl[[0, 1, 3]] & 0x80).any()
+        assert int(plane.state.len[2]) == int(len_before[2])
+        with pytest.raises(DegenerateRowError):
+            plane.to_decisions(d, 0)
+        dec = plane.to_decisions(d, 0, raise_degenerate=False)
+        assert dec[2] is None and all(dec[b] is not None for b in (0, 1, 3))
