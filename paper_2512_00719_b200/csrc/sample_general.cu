@@ -76,6 +76,24 @@ DP_DEV void smem_add_u64(unsigned long long* addr, unsigned long long w) {
   if (up) atomicAdd(p + 1, up);
 }
 
+// Every element of a row domain, 16-byte vector loads (8 bf16 / 4 f32 per
+// load; the passes re-read the row from L2): fn(position, value).
+template <typename T, typename F>
+DP_DEV void for_each_elem(const T* rowp, int64_t n, uint32_t tid, F fn) {
+  constexpr int EPV = Elem<T>::kPerVec;
+  const uintptr_t addr = reinterpret_cast<uintptr_t>(rowp);
+  const int64_t a0 = min64(n, (int64_t)(((16u - (addr & 15u)) & 15u) / sizeof(T)));
+  for (int64_t i = tid; i < a0; i += kGenNT) fn(i, Elem<T>::get(rowp, i));
+  const int64_t nvec = (n - a0) / EPV;
+  const uint4* vp = reinterpret_cast<const uint4*>(rowp + a0);
+  for (int64_t v = tid; v < nvec; v += kGenNT) {
+    const uint4 q = __ldg(vp + v);
+#pragma unroll
+    for (int e = 0; e < EPV; ++e) fn(a0 + v * EPV + e, vec_elem<T>(q, e));
+  }
+  for (int64_t i = a0 + nvec * EPV + tid; i < n; i += kGenNT) fn(i, Elem<T>::get(rowp, i));
+}
+
 // block reductions over kGenNT threads
 template <typename F>
 DP_DEV double blk_sum_d(double v, GenSmem& g, F sync) {
@@ -228,8 +246,9 @@ __global__ void __launch_bounds__(kGenNT, 1) general_sample_kernel(SampleArgs a)
 
   // ---- pass A: max of unpenalised values
   float mx = -INFINITY;
-  for (int64_t i = tid; i < n; i += kGenNT)
-    if (!is_pen(i)) mx = fmaxf(mx, val(i));
+  for_each_elem(rowp, n, tid, [&](int64_t i, float x) {
+    if (!is_pen(i)) mx = fmaxf(mx, x);
+  });
   mx = blk_max_f(mx, g, sync);
   double rmax = mx == -INFINITY ? -INFINITY : ready_plain(mx, p);
   {
@@ -326,9 +345,8 @@ __global__ void __launch_bounds__(kGenNT, 1) general_sample_kernel(SampleArgs a)
   sync();
   unsigned long long wsum = 0, wminp = 0;
   uint32_t cminp = 0, cnp = 0;
-  for (int64_t i = tid; i < n; i += kGenNT) {
-    if (is_pen(i)) continue;
-    const float x = val(i);
+  for_each_elem(rowp, n, tid, [&](int64_t i, float x) {
+    if (is_pen(i)) return;
     const uint32_t b = bucket_of(x);
     const unsigned long long w = wfix(x);
     atomicAdd(&g.cnt[b], 1u);
@@ -339,7 +357,7 @@ __global__ void __launch_bounds__(kGenNT, 1) general_sample_kernel(SampleArgs a)
       wminp += w;
       ++cminp;
     }
-  }
+  });
   for (uint32_t j = tid; j < np; j += kGenNT) {
     atomicAdd(&g.cnt[pen[j].bucket], 1u);
     smem_add_u64(&g.mass[pen[j].bucket], pen[j].wfp);
@@ -447,19 +465,18 @@ __global__ void __launch_bounds__(kGenNT, 1) general_sample_kernel(SampleArgs a)
       auto member = [&](unsigned long long k, uint32_t b) -> bool {
         return (use_bucket ? b == (uint32_t)bsel : true) && (k & pmask) == pref && in_range(k);
       };
-      for (int64_t i = tid; i < n; i += kGenNT) {
-        if (is_pen(i)) continue;
-        const float x = val(i);
+      for_each_elem(rowp, n, tid, [&](int64_t i, float x) {
+        if (is_pen(i)) return;
         const uint32_t b = bucket_of(x);
-        if (b != (uint32_t)bsel) continue;
+        if (b != (uint32_t)bsel) return;
         const unsigned long long k = ekey(i, x);
-        if (!member(k, b)) continue;
+        if (!member(k, b)) return;
         const uint32_t d = (uint32_t)(k >> shift) & 2047u;
         // descending key order: digit 2047 first
         atomicAdd(&g.digit_cnt[2047u - d], 1u);
         const unsigned long long w = wfix(x);
         if (w) smem_add_u64(&g.digit_mass[2047u - d], w);
-      }
+      });
       for (uint32_t j = tid; j < np; j += kGenNT) {
         const unsigned long long k = pen[j].vkey;
         if (pen[j].bucket == (uint32_t)bsel && member(k, pen[j].bucket)) {
@@ -494,18 +511,17 @@ __global__ void __launch_bounds__(kGenNT, 1) general_sample_kernel(SampleArgs a)
     // collect the range: unpenalised + penalised members
     if (tid == 0) g.ncol = 0u;
     sync();
-    for (int64_t i = tid; i < n; i += kGenNT) {
-      if (is_pen(i)) continue;
-      const float x = val(i);
-      if (bucket_of(x) != (uint32_t)bsel) continue;
+    for_each_elem(rowp, n, tid, [&](int64_t i, float x) {
+      if (is_pen(i)) return;
+      if (bucket_of(x) != (uint32_t)bsel) return;
       const unsigned long long k = ekey(i, x);
-      if (!in_range(k)) continue;
+      if (!in_range(k)) return;
       const uint32_t s = atomicAdd(&g.ncol, 1u);
       if (s < (uint32_t)kCollect) {
         g.ckey[s] = k;
         g.cw[s] = wfix(x);
       }
-    }
+    });
     for (uint32_t j = tid; j < np; j += kGenNT) {
       if (pen[j].bucket == (uint32_t)bsel && in_range(pen[j].vkey)) {
         const uint32_t s = atomicAdd(&g.ncol, 1u);
