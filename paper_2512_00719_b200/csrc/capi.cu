@@ -136,10 +136,18 @@ Launches plan_launches(dp::SampleArgs& a, const dp_plan_t* plan, int mode, int64
   const bool all_warp = a.use_warp && bounded && kmax <= dp::kWarpKMax && cap <= dp::kWarpPenCap &&
                         (kmax + cap <= dp::kWarpKpMax || n <= dp::kWarpKpMax);
   const int64_t kp_topk = kmax + (mode == dp::kHot ? 0 : cap);
-  const bool all_topk = bounded && (kp_topk < n ? kp_topk : n) <= a.kcap && kmax + 2 * cap <= a.lcap;
+  const bool k_rows_fit = kmax > 0 && kmax < n && (kp_topk < n ? kp_topk : n) <= a.kcap && kmax + 2 * cap <= a.lcap;
+  const bool all_topk = bounded && k_rows_fit;
+  // top-k-off rows present (kmin == 0): they are nucleus rows of the top-k
+  // kernel (the general kernel then only sees the fallback list) when the
+  // nucleus list fits; rows with top-k on fit by k_rows_fit
+  const int64_t kp_nuc = dp::kNucK + (mode == dp::kHot ? 0 : cap);
+  const bool nuc_all = a.fb_rows != nullptr && n >= 2 * (int64_t)dp::kNucK && kp_nuc <= a.kcap &&
+                       dp::kNucK + 2 * cap <= a.lcap;
+  const bool mixed_topk = kmin == 0 && k_rows_fit && nuc_all;
   L.warp = a.use_warp != 0;
   L.topk = !all_warp;
-  L.general = !(all_warp || all_topk);
+  L.general = !(all_warp || all_topk || mixed_topk);
   return L;
 }
 
