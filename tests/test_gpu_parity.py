@@ -455,3 +455,32 @@ def test_degenerate_rows_are_flagged_and_raised(torch_cuda):
             plane.to_decisions(d, 0)
         dec = plane.to_decisions(d, 0, raise_degenerate=False)
         assert dec[2] is None and all(dec[b] is not None for b in (0, 1, 3))
+
+
+def test_multi_wave_mixed_batch_matches_oracle(torch_cuda):
+    """A batch of more than two waves of resident CTAs mixing top-k, nucleus
+    and fallback rows (general kernel), checked against the oracle on a row
+    sample."""
+    torch = torch_cuda
+    v, bsz = 4096, 320
+    kinds = [dict(temperature=0.8, top_k=50, top_p=0.9, min_p=0.05, rep_penalty=1.1, presence_penalty=0.5,
+                  frequency_penalty=0.1), dict(temperature=0.7, top_p=0.9), dict(temperature=9.0),
+             dict(temperature=1.0, top_k=1), dict(temperature=0.8, min_p=0.05, rep_penalty=1.3)]
+    params = [O.Params(**kinds[b % len(kinds)], seed=b) for b in range(bsz)]
+    prompts = [np.random.default_rng(500 + b).integers(0, v, 24) for b in range(bsz)]
+    states = [O.State.new(p, v) for p in prompts]
+    src = O.Synthetic(v)
+    plane = plane_for(torch, v, params, prompts)
+    check = list(range(0, bsz, 7))
+    exempt = []
+    for it in range(2):
+        x = src.wire(it, range(bsz))
+        d = plane.sample(torch.from_numpy(x).cuda(), it, update=False)
+        tok, lp = d.token.cpu().numpy(), d.logprob.cpu().numpy()
+        dec = [O.sample_full_row(x[b], states[b], params[b], O.uniforms_per_row([params[b].seed], it, [b])[0])
+               for b in check]
+        compare(f"mixed/it{it}", tok[check], lp[check], dec, exempt, lp_tol=1e-6)
+        for b in range(bsz):
+            states[b].update(int(tok[b]))
+        plane.state.update(d.token)
+    print("exemptions:", exempt)
