@@ -99,6 +99,11 @@ DP_DEV uint4 ld_stream16(const void* p) {
                : "l"(p));
   return r;
 }
+// L2 bulk prefetch (TMA engine, no registers, no completion to wait for):
+// pulls a future chunk of the row into L2 so its loads hit there
+DP_DEV void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
 template <typename T> DP_DEV float vec_elem(const uint4& v, int e);
 template <> DP_DEV float vec_elem<float>(const uint4& v, int e) {
   uint32_t w = e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w;

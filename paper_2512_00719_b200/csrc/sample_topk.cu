@@ -85,6 +85,11 @@ __host__ __device__ inline TopkLayout topk_layout(int ccap, int kcap, int lcap, 
 
 // NUC: the call may hold nucleus rows (top-k off); the plain top-k
 // instantiation carries none of that code
+#ifndef DP_PREFETCH
+#define DP_PREFETCH 1
+#endif
+constexpr int kPrefetch = DP_PREFETCH;   // L2 prefetch distance, in batches
+
 template <typename T, int MODE, int NT, int U, bool NUC>
 __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample_kernel(SampleArgs a) {
   constexpr int NW = NT / 32;
@@ -279,6 +284,11 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
   const int32_t base0 = v_lo + (int32_t)warp * 32 * U;
   for (int pass_no = 0;; ++pass_no) {
     int32_t base = base0;
+    if (lane == 0) {   // the first kPrefetch chunks after the first batch -> L2
+#pragma unroll
+      for (int d = 1; d <= kPrefetch; ++d)
+        if (base + d * NT * U + 32 * U <= v_hi) prefetch_l2(vp + base + d * NT * U, 32u * U * 16u);
+    }
     uint4 v[U];
 #pragma unroll
     for (int j = 0; j < U; ++j) {
@@ -390,6 +400,9 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
       }
       base += NT * U;
       if (base >= v_hi) break;
+      // this warp's chunk kPrefetch iterations ahead -> L2 (one lane, 4 KB)
+      if (lane == 0 && base + kPrefetch * NT * U + 32 * U <= v_hi)
+        prefetch_l2(vp + base + kPrefetch * NT * U, 32u * U * 16u);
       if (base + 32 * U <= v_hi) {   // full batch: unpredicated loads at immediate offsets
         const uint4* q = vp + base + (int32_t)lane;
 #pragma unroll
