@@ -191,27 +191,45 @@ def _port_worker(args):
     return n, time.perf_counter() - t0
 
 
-def cpu_baseline(x_rows: np.ndarray, prompts, params, seconds: float, cores: int | None = None):
+class CpuBaseline:
     """The reference CPU sampler timed on this host's cores: one process per
     core (the reference's m-sampler design, service.py:584-589, without the
-    GIL), rows split by partition_batch (transport.py:133-144).  Uses the
-    unmodified reference from baseline/_ref when installed ("reference"), else
-    the oracle port ("port").  Returns (tokens/s, processes, rows, kind)."""
-    import multiprocessing as mp
+    GIL), rows split by partition_batch (transport.py:133-144), one process
+    pool reused across measurements.  Uses the unmodified reference from
+    baseline/_ref when installed ("reference"), else the oracle port ("port")."""
 
-    cores = cores or len(os.sched_getaffinity(0))
-    kind = "reference" if reference_available() else "port"
-    worker = _ref_worker if kind == "reference" else _port_worker
-    idx = np.arange(x_rows.shape[0])
-    parts = [idx[lo:hi] for lo, hi in _partition(x_rows.shape[0], min(cores, x_rows.shape[0]))]
-    jobs = [(x_rows[p], [prompts[i] for i in p], params, int(p[0]), seconds) for p in parts if len(p)]
-    ctx = mp.get_context("fork")
-    with ctx.Pool(len(jobs)) as pool:
-        res = pool.map(worker, jobs)
-    rows = sum(r[0] for r in res)
-    # every process decides its rows concurrently: aggregate rate = sum of per-process rates
-    rate = sum(r[0] / r[1] for r in res if r[1] > 0)
-    return rate, len(jobs), rows, kind
+    def __init__(self, x_rows: np.ndarray, prompts, params, cores: int | None = None):
+        import multiprocessing as mp
+
+        cores = cores or len(os.sched_getaffinity(0))
+        self.kind = "reference" if reference_available() else "port"
+        self.worker = _ref_worker if self.kind == "reference" else _port_worker
+        idx = np.arange(x_rows.shape[0])
+        parts = [idx[lo:hi] for lo, hi in _partition(x_rows.shape[0], min(cores, x_rows.shape[0]))]
+        self.parts = [(x_rows[p], [prompts[i] for i in p], params, int(p[0])) for p in parts if len(p)]
+        self.pool = mp.get_context("fork").Pool(len(self.parts))
+
+    def measure(self, seconds: float):
+        """(tokens/s, processes, rows decided) over about `seconds` of work."""
+        res = self.pool.map(self.worker, [job + (seconds,) for job in self.parts])
+        rows = sum(r[0] for r in res)
+        # every process decides its rows concurrently: aggregate rate = sum of per-process rates
+        rate = sum(r[0] / r[1] for r in res if r[1] > 0)
+        return rate, len(self.parts), rows
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+
+
+def cpu_baseline(x_rows: np.ndarray, prompts, params, seconds: float, cores: int | None = None):
+    """One measurement with a fresh pool.  Returns (tokens/s, processes, rows, kind)."""
+    cb = CpuBaseline(x_rows, prompts, params, cores)
+    try:
+        rate, procs, rows = cb.measure(seconds)
+    finally:
+        cb.close()
+    return rate, procs, rows, cb.kind
 
 
 def _partition(n, m):
@@ -236,16 +254,23 @@ def reference_arm(args, cfg):
     x = src.wire(0, range(nrows))
     prompts = [np.random.default_rng(b).integers(0, v, PROMPT_LEN) for b in range(nrows)]
     steps = []
-    # bounded: the whole --steps K --warmup W run stays within ~ref_budget seconds
-    per_step = max(0.25, min(args.ref_seconds, args.ref_budget / max(1, args.steps + args.warmup)))
-    for _ in range(args.warmup):
-        cpu_baseline(x, prompts, cfg["params"], per_step)
-    total_rows, total_t = 0, 0.0
-    for _ in range(args.steps):
-        rate, cores, rows, kind = cpu_baseline(x, prompts, cfg["params"], per_step)
-        steps.append(rate)
-        total_rows += rows
-        total_t += rows / rate
+    # bounded: the whole --steps K --warmup W run stays within ~ref_budget
+    # seconds (one process pool; every step decides each process's rows at
+    # least once)
+    per_step = max(0.02, min(args.ref_seconds, args.ref_budget / max(1, args.steps + args.warmup)))
+    cb = CpuBaseline(x, prompts, cfg["params"])
+    kind = cb.kind
+    try:
+        for _ in range(args.warmup):
+            cb.measure(per_step)
+        total_rows, total_t = 0, 0.0
+        for _ in range(args.steps):
+            rate, cores, rows = cb.measure(per_step)
+            steps.append(rate)
+            total_rows += rows
+            total_t += rows / rate
+    finally:
+        cb.close()
     value = total_rows / total_t
     what = ("unmodified reference (baseline/_ref) _Sampler('offload-truncate').sample + "
             "update_output_histogram, producer make_shard_blocks untimed as in harness.py:255-279"
