@@ -529,7 +529,11 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
 
 template <typename T, int MODE, bool NUC>
 static cudaError_t launch_topk_t(const SampleArgs& a, int grid_rows, cudaStream_t st) {
-  constexpr int U = 8, NT = 256;
+#ifndef DP_TOPK_NT
+#define DP_TOPK_NT 256
+#define DP_TOPK_U 8
+#endif
+  constexpr int U = DP_TOPK_U, NT = DP_TOPK_NT;
   const int64_t n = MODE == kFull ? a.V : (MODE == kHot ? a.H : a.V - a.H);
   const int bm_words = MODE == kHot ? (int)((n + 31) / 32) + 1 : 0;
   const TopkLayout L = topk_layout<NT>(a.wcap, a.kcap, a.lcap, bm_words, a.split);
