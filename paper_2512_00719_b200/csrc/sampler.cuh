@@ -217,7 +217,7 @@ DP_DEV DrawResult warp_filter_draw_smem(const double* r, int32_t k, const dp_par
   }
   __syncwarp();
   int32_t kept = k;
-  double margin = 1e300;
+  double margin = 1e30;
   const double total = cum[k - 1];
   if (p.top_p < 1.0) {                               // filtering.py:91-95
     const double thr = p.top_p * total;
@@ -229,7 +229,7 @@ DP_DEV DrawResult warp_filter_draw_smem(const double* r, int32_t k, const dp_par
     const int32_t kp = below + 1;
     kept = min(kept, kp);
     for (int32_t j = max(0, kp - 2); j < min(k, kp + 1); ++j) margin = fmin(margin, fabs(cum[j] - thr));
-    margin /= total;
+    margin = (double)__fdividef((float)margin, (float)total);   // flag only: f32 ratio
   }
   if (p.min_p > 0.0) {                               // filtering.py:96-98
     const double floor_ = p.min_p * w[0];
@@ -256,45 +256,54 @@ DP_DEV DrawResult warp_filter_draw_smem(const double* r, int32_t k, const dp_par
   DrawResult res;
   res.index = js;
   res.kept = kept;
-  res.logprob = log(w[js] / S);
-  res.margin = fmin(margin, dm / S);
+  res.logprob = (r[js] - r0) - log(S);   // ln(w_j / S), w_j = exp(r_j - r_0)
+  res.margin = fmin(margin, (double)__fdividef((float)dm, (float)S));
   return res;
 }
 
 // k <= 64: everything in registers (two candidates per lane)
 DP_DEV DrawResult warp_filter_draw_reg(const double* r, int32_t k, const dp_params_t& p, double u) {
+  // compact on purpose: this runs once per row with a cold instruction cache,
+  // so every instruction it does not have is ~20 cycles saved
   const uint32_t lane = lane_id();
   const int32_t j0 = lane, j1 = lane + 32;
   const double r0 = __shfl_sync(0xffffffffu, r[0], 0);
-  const double ra = j0 < k ? r[j0] : 0.0, rb = j1 < k ? r[j1] : 0.0;
-  const double wa = j0 < k ? exp(ra - r0) : 0.0;
-  const double wb = j1 < k ? exp(rb - r0) : 0.0;
+  double rr[2], ww[2];
+#pragma unroll 1
+  for (int h = 0; h < 2; ++h) {   // one copy of the f64 exp
+    const int32_t j = (int32_t)lane + 32 * h;
+    rr[h] = j < k ? r[j] : 0.0;
+    ww[h] = j < k ? exp(rr[h] - r0) : 0.0;
+  }
+  const double ra = rr[0], rb = rr[1], wa = ww[0], wb = ww[1];
   const double ca = warp_incl_scan(wa);
   const double tot_a = __shfl_sync(0xffffffffu, ca, 31);
   const double cb = warp_incl_scan(wb) + tot_a;
   const double total = __shfl_sync(0xffffffffu, cb, 31);
-  // value at global index j (any lane): cum / w via shuffles
-  auto cum_at = [&](int32_t j) -> double {
-    const double x = __shfl_sync(0xffffffffu, j < 32 ? ca : cb, j & 31);
-    return x;
-  };
+  // value at global index j (any lane): cum / w / r via shuffles
+  auto cum_at = [&](int32_t j) -> double { return __shfl_sync(0xffffffffu, j < 32 ? ca : cb, j & 31); };
   auto w_at = [&](int32_t j) -> double { return __shfl_sync(0xffffffffu, j < 32 ? wa : wb, j & 31); };
+  auto r_at = [&](int32_t j) -> double { return __shfl_sync(0xffffffffu, j < 32 ? ra : rb, j & 31); };
+  // margins only feed the 1e-6 boundary flag: f32 ratios are plenty
+  auto ratio = [](double a, double b) -> double { return (double)__fdividef((float)a, (float)b); };
   int32_t kept = k;
-  double margin = 1e300;
+  double margin = 1e30;
   if (p.top_p < 1.0) {
     const double thr = p.top_p * total;
     const int32_t below = __popc(__ballot_sync(0xffffffffu, j0 < k && ca < thr)) +
                           __popc(__ballot_sync(0xffffffffu, j1 < k && cb < thr));
     const int32_t kp = below + 1;
     kept = min(kept, kp);
+#pragma unroll 1
     for (int32_t j = max(0, kp - 2); j < min(k, kp + 1); ++j) margin = fmin(margin, fabs(cum_at(j) - thr));
-    margin /= total;
+    margin = ratio(margin, total);
   }
   if (p.min_p > 0.0) {
     const double floor_ = p.min_p * 1.0;   // w_0 = exp(0) = 1
     const int32_t ge = __popc(__ballot_sync(0xffffffffu, j0 < k && wa >= floor_)) +
                        __popc(__ballot_sync(0xffffffffu, j1 < k && wb >= floor_));
     kept = min(kept, ge);
+#pragma unroll 1
     for (int32_t j = max(0, ge - 1); j < min(k, ge + 1); ++j) margin = fmin(margin, fabs(w_at(j) - floor_));
   }
   kept = max(1, kept);
@@ -308,8 +317,9 @@ DP_DEV DrawResult warp_filter_draw_reg(const double* r, int32_t k, const dp_para
   DrawResult res;
   res.index = js;
   res.kept = kept;
-  res.logprob = log(w_at(js) / S);
-  res.margin = fmin(margin, dm / S);
+  // ln p_j = ln(w_j / S) = (r_j - r_0) - ln S (w_j = exp(r_j - r_0))
+  res.logprob = (r_at(js) - r0) - log(S);
+  res.margin = fmin(margin, ratio(dm, S));
   return res;
 }
 
@@ -336,7 +346,7 @@ DP_DEV DrawResult warp_filter_draw_nuc(const double* r, int32_t K, const dp_para
   __syncwarp();
   fallback = false;
   int32_t kept = K;
-  double margin = 1e300;
+  double margin = 1e30;
   const bool neutral = !(p.top_p < 1.0) && !(p.min_p > 0.0);
   bool p_open = false, m_open = false;
   if (p.top_p < 1.0) {                               // filtering.py:91-95 over the whole domain
@@ -350,7 +360,7 @@ DP_DEV DrawResult warp_filter_draw_nuc(const double* r, int32_t K, const dp_para
     const int32_t kp = below + 1;
     kept = min(kept, kp);
     for (int32_t j = max(0, kp - 2); j < min(K, kp + 1); ++j) margin = fmin(margin, fabs(cum[j] - thr));
-    margin /= total;
+    margin = (double)__fdividef((float)margin, (float)total);   // flag only: f32 ratio
   }
   if (p.min_p > 0.0) {                               // filtering.py:96-98
     const double floor_ = p.min_p;                   // w_0 = 1
@@ -381,8 +391,8 @@ DP_DEV DrawResult warp_filter_draw_nuc(const double* r, int32_t K, const dp_para
   DrawResult res;
   res.index = js;
   res.kept = kept;
-  res.logprob = log(w[js] / S);
-  res.margin = fmin(margin, dm / S);
+  res.logprob = (r[js] - r0) - log(S);   // ln(w_j / S), w_j = exp(r_j - r_0)
+  res.margin = fmin(margin, (double)__fdividef((float)dm, (float)S));
   return res;
 }
 
