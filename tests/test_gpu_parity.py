@@ -484,3 +484,45 @@ def test_multi_wave_mixed_batch_matches_oracle(torch_cuda):
             states[b].update(int(tok[b]))
         plane.state.update(d.token)
     print("exemptions:", exempt)
+
+
+@pytest.mark.parametrize("storage", ["whole", "split_host"])
+def test_shvs_bf16_rows_match_oracle(torch_cuda, storage):
+    """SHVS on bf16 logits (C5's wire type; values upcast exactly to f32 for
+    the oracle), whole rows and split storage with a pinned-host tail, mixed
+    filters and penalties, forced rejections from a cold hot set."""
+    torch = torch_cuda
+    v, bsz = 8192, 40
+    kinds = [dict(temperature=0.8, top_k=1), dict(temperature=0.8, top_k=50), dict(temperature=0.8, top_p=0.9),
+             dict(temperature=0.8, min_p=0.05),
+             dict(temperature=0.8, top_k=50, top_p=0.9, min_p=0.05, rep_penalty=1.1, presence_penalty=0.5,
+                  frequency_penalty=0.1)]
+    params = [O.Params(**kinds[b % len(kinds)], seed=b) for b in range(bsz)]
+    prompts = [np.random.default_rng(700 + b).integers(0, v, 24) for b in range(bsz)]
+    states = [O.State.new(p, v) for p in prompts]
+    src = O.Synthetic(v)
+    hot_ids = src.rank_to_token[::-1][:1024].copy()      # cold hot set: many rejections
+    tail = O.tail_ids_of(hot_ids, v)
+    plane = plane_for(torch, v, params, prompts, hot_ids=hot_ids)
+    exempt = []
+    for it in range(3):
+        xb = torch.from_numpy(src.wire(it, range(bsz))).bfloat16()
+        x = xb.float().numpy()
+        xt = plane.hot.to_hot_first(xb.cuda()).contiguous()
+        summ = plane.row_summary(xt, inv_perm=plane.hot.device_maps(plane.device)[1])
+        if storage == "whole":
+            d = plane.sample(xt, it, variant="shvs", summary=summ, update=False)
+        else:
+            h = plane.hot.size
+            d = plane.sample_split(xt[:, :h].contiguous(), xt[:, h:].contiguous().cpu().pin_memory(), it, summ,
+                                   update=False)
+        tok, lp = d.token.cpu().numpy(), d.logprob.cpu().numpy()
+        dec = [O.sample_shvs_row(x[b], states[b], params[b], O.uniforms_per_row([params[b].seed], it, [b])[0],
+                                 hot_ids, tail) for b in range(bsz)]
+        compare(f"bf16-shvs/{storage}/it{it}", tok, lp, dec, exempt, lp_tol=1e-6)
+        acc = (d.flags.cpu().numpy() & 0x02) != 0
+        assert (~acc).sum() > 0   # the tail pass ran
+        for b in range(bsz):
+            states[b].update(int(dec[b].token))
+        plane.state.update(torch.from_numpy(np.array([dd.token for dd in dec], np.int32)).cuda())
+    print("exemptions:", exempt)
