@@ -145,6 +145,23 @@ DP_API int dp_sample_full(const void* logits, int dtype, int64_t B, int64_t V, i
                    int32_t* token, double* logprob, uint8_t* flags,
                    const dp_debug_t* debug_host, const dp_plan_t* plan_host, void* stream);
 
+/* TP-sharded logits, read in place (replaces AssembledLogitsView +
+ * assemble_view, transport.py:460-557): the t vocab shards of equal width
+ * W = V / t tile [0, V); row b of shard s (vocab [s*W, (s+1)*W)) is at
+ * shards[s] + b * ld elements (ld >= W; the reference's (W, B) Fortran-order
+ * LogitsShardBlock.values, core.py:185-201, is exactly this layout).
+ * shards is a HOST array of t <= 8 device pointers (peer memory of other TP
+ * ranks works once peer access is enabled).  One cluster of t CTAs decides a
+ * row, CTA s streaming shard s; results equal dp_sample_full on the stitched
+ * rows.  Rows must all carry top-k: plan->min_top_k > 0 and plan->max_top_k
+ * within the top-k kernel's capacity, else DP_ERR_UNSUPPORTED (stitch and
+ * call dp_sample_full).  Bad tiling -> DP_ERR_ARG (IncompleteIterationError). */
+DP_API int dp_sample_full_sharded(const void* const* shards, int32_t t, int dtype, int64_t B, int64_t V,
+                   int64_t ld, const dp_params_t* params, const dp_penalty_t* pen_host,
+                   const double* uniforms, const uint64_t* seq_ids, uint64_t iteration,
+                   int32_t* token, double* logprob, uint8_t* flags,
+                   const dp_debug_t* debug_host, const dp_plan_t* plan_host, void* stream);
+
 /* Producer summary: make_shard_blocks' per-row (row_max, total_expsum) over the
  * penalized, temperature-scaled row (service.py:470-504, shvs.py:157-168).
  * Layout-agnostic (a permutation does not change max or sum). */

@@ -26,7 +26,7 @@ EXPORTS = [
     "dp_version", "dp_device_check", "dp_last_error", "dp_uniforms", "dp_sample_full",
     "dp_row_summary", "dp_sample_shvs", "dp_penalty_update", "dp_penalty_reset",
     "dp_ready_rows", "dp_synth_logits", "dp_hot_mass_curve", "dp_row_summary_raw", "dp_sample_shvs_split",
-    "dp_stage_hot",
+    "dp_stage_hot", "dp_sample_full_sharded",
 ]
 
 
@@ -87,6 +87,9 @@ _SIGS = {
                         _P, _P, _U64, _P, _P, _P, C.POINTER(Debug), C.POINTER(Plan), _P, _P], C.c_int),
     "dp_sample_shvs_split": ([_P, _I64, _P, _I64, C.c_int, _I64, _I64, _I64, _P, _P, _P, _P, _P, C.POINTER(Penalty),
                               _P, _P, _U64, _P, _P, _P, C.POINTER(Debug), C.POINTER(Plan), _P, _P], C.c_int),
+    "dp_sample_full_sharded": ([C.POINTER(C.c_void_p), C.c_int32, C.c_int, _I64, _I64, _I64, _P,
+                                C.POINTER(Penalty), _P, _P, _U64, _P, _P, _P, C.POINTER(Debug), C.POINTER(Plan),
+                                _P], C.c_int),
     "dp_stage_hot": ([_P, _I64, C.c_int, _I64, _I64, _P, _I64, _P], C.c_int),
     "dp_penalty_update": ([C.POINTER(Penalty), _P, _I64, _P, _P], C.c_int),
     "dp_penalty_reset": ([C.POINTER(Penalty), _I64, _P], C.c_int),

@@ -261,6 +261,53 @@ int dp_sample_full(const void* logits, int dtype, int64_t B, int64_t V, int64_t 
   return DP_OK;
 }
 
+int dp_sample_full_sharded(const void* const* shards, int32_t t, int dtype, int64_t B, int64_t V, int64_t ld,
+                           const dp_params_t* params, const dp_penalty_t* pen_host, const double* uniforms,
+                           const uint64_t* seq_ids, uint64_t iteration, int32_t* token, double* logprob,
+                           uint8_t* flags, const dp_debug_t* debug_host, const dp_plan_t* plan_host, void* stream) {
+  if (!shards || !params || !token || !logprob || !flags)
+    return fail(DP_ERR_ARG, "dp_sample_full_sharded: null argument%s");
+  if (!uniforms && !seq_ids) return fail(DP_ERR_ARG, "dp_sample_full_sharded: need uniforms or seq_ids%s");
+  if (dtype != DP_F32 && dtype != DP_BF16) return fail(DP_ERR_UNSUPPORTED, "dp_sample_full_sharded: dtype%s");
+  if (t < 1 || t > dp::kMaxShards) return fail(DP_ERR_ARG, "dp_sample_full_sharded: shard count outside [1, 8]%s");
+  // equal-width tiling from 0 (AssembledLogitsView.__post_init__, transport.py:474-489)
+  if (B < 0 || V < 1 || V % t != 0 || ld < V / t || V >= (1ll << 31))
+    return fail(DP_ERR_ARG, "dp_sample_full_sharded: shards do not tile [0, V) with equal widths%s");
+  for (int32_t s = 0; s < t; ++s)
+    if (!shards[s]) return fail(DP_ERR_ARG, "dp_sample_full_sharded: null shard%s");
+  if (!valid_pen(pen_host, V)) return fail(DP_ERR_ARG, "dp_sample_full_sharded: penalty state does not match V%s");
+  if (B == 0) return DP_OK;
+  dp::SampleArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.logits = shards[0];
+  a.ld = ld;
+  a.V = V;
+  a.H = V;
+  a.params = params;
+  a.pen = *pen_host;
+  a.uniforms = uniforms;
+  a.seq_ids = seq_ids;
+  a.iteration = iteration;
+  a.n_rows = (int32_t)B;
+  a.token = token;
+  a.logprob = logprob;
+  a.flags = flags;
+  if (debug_host) a.dbg = *debug_host;
+  plan_topk(a, plan_host, B, V, dtype == DP_F32 ? 4 : 2);
+  a.split = t;   // cluster rank s streams shard s in place
+  a.nshard = t;
+  a.shard_n = V / t;
+  for (int32_t s = 0; s < t; ++s) a.shard[s] = shards[s];
+  // zero-copy only through the top-k kernel: every row must carry top-k
+  // within the plan's bounds (the other kernels read contiguous rows)
+  const Launches L = plan_launches(a, plan_host, dp::kFull, B, V, false);
+  if (use_stream(B, plan_host) || L.warp || L.general || !L.topk)
+    return fail(DP_ERR_UNSUPPORTED,
+                "dp_sample_full_sharded: needs plan min_top_k > 0 and max_top_k within the top-k kernel's "
+                "capacity (stitch the shards and call dp_sample_full otherwise)%s");
+  return cuda_status(dp::launch_topk(a, dtype, dp::kFull, (int)B, (cudaStream_t)stream), "dp_sample_full_sharded");
+}
+
 int dp_row_summary(const void* logits, int dtype, int64_t B, int64_t V, int64_t ld, const dp_params_t* params,
                    const dp_penalty_t* pen_host, const int32_t* inv_perm, double* row_max, double* total_expsum,
                    void* stream) {

@@ -63,7 +63,7 @@ DP_DEV PenPrefetch pen_prefetch(const SampleArgs& a, int row, int32_t plen, cons
       const int64_t pos = id_to_pos(a, pids[j]) - lo;
       if (pos >= 0 && pos < n) {
         pp.pos[i] = (int32_t)pos;
-        pp.x[i] = Elem<T>::get(rowp, pos);
+        pp.x[i] = dom_value<T>(a, row, rowp, pos);
         pp.cnt[i] = pcnt[j];
       }
     }
@@ -280,7 +280,7 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
     }
     const int64_t q = id_to_pos(a, pids[j]) - lo;
     pos = (q >= 0 && q < n) ? (int32_t)q : -1;
-    x = pos >= 0 ? Elem<T>::get(rowp, q) : 0.f;
+    x = pos >= 0 ? dom_value<T>(a, row, rowp, q) : 0.f;
     c = pcnt[j];
   };
 

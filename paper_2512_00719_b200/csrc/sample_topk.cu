@@ -174,14 +174,21 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
 
   lapk(17);
   // ---- segment geometry (32-bit vector indices: V < 2^31)
-  const uintptr_t addr = reinterpret_cast<uintptr_t>(rowp);
-  const int32_t a0 = (int32_t)min64(n, (int64_t)(((16u - (addr & 15u)) & 15u) / sizeof(T)));
-  const int32_t nvec = (int32_t)((n - a0) / EPV);
+  // TP-sharded rows: this CTA's segment is its own vocab shard, read in place
+  // (positions offset by pos0); otherwise a vector-aligned chunk of the row
+  const bool sharded = MODE == kFull && a.nshard > 0;
+  const T* segp = sharded ? reinterpret_cast<const T*>(a.shard[rank]) + (int64_t)row * a.ld : rowp;
+  const int64_t n_seg = sharded ? a.shard_n : n;
+  const uint32_t pos0 = sharded ? rank * (uint32_t)a.shard_n : 0u;
+  const bool own_scal = rank == 0 || sharded;   // this CTA holds scalar head / tail elements
+  const uintptr_t addr = reinterpret_cast<uintptr_t>(segp);
+  const int32_t a0 = (int32_t)min64(n_seg, (int64_t)(((16u - (addr & 15u)) & 15u) / sizeof(T)));
+  const int32_t nvec = (int32_t)((n_seg - a0) / EPV);
   const int32_t tail0 = a0 + nvec * EPV;
-  const int32_t chunk = ((nvec + (int32_t)split - 1) / (int32_t)split + 31) & ~31;
-  const int32_t v_lo = min(nvec, (int32_t)rank * chunk);
+  const int32_t chunk = sharded ? nvec : ((nvec + (int32_t)split - 1) / (int32_t)split + 31) & ~31;
+  const int32_t v_lo = sharded ? 0 : min(nvec, (int32_t)rank * chunk);
   const int32_t v_hi = min(nvec, v_lo + chunk);
-  const uint4* vp = reinterpret_cast<const uint4*>(rowp + a0);
+  const uint4* vp = reinterpret_cast<const uint4*>(segp + a0);
   uint4* cvec = reinterpret_cast<uint4*>(cand);                 // admitted vectors
   int32_t* cidx = reinterpret_cast<int32_t*>(cvec + ccap);      // their vector index
   const T* celem = reinterpret_cast<const T*>(cvec);
@@ -243,16 +250,16 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
   // scalar head / tail elements (at most 2*EPV-2) belong to CTA 0 (warp 0)
   auto head_tail = [&](bool first) {
     const int32_t hi_i = lane, ti = tail0 + lane;
-    const bool hv = hi_i < a0, tv = ti < n;
-    const float hx = hv ? Elem<T>::get(rowp, hi_i) : -INFINITY;
-    const float tx = tv ? Elem<T>::get(rowp, ti) : -INFINITY;
+    const bool hv = hi_i < a0, tv = ti < n_seg;
+    const float hx = hv ? Elem<T>::get(segp, hi_i) : -INFINITY;
+    const float tx = tv ? Elem<T>::get(segp, ti) : -INFINITY;
     if (first && hv) accum(hx, hi_i);
     if (first && tv) accum(tx, ti);
-    const bool hp = hv && !pen_bit(hi_i) && comp_key(hx, (uint32_t)hi_i) >= thr;
-    const bool tp = tv && !pen_bit(ti) && comp_key(tx, (uint32_t)ti) >= thr;
+    const bool hp = hv && !pen_bit(hi_i) && comp_key(hx, pos0 + (uint32_t)hi_i) >= thr;
+    const bool tp = tv && !pen_bit(ti) && comp_key(tx, pos0 + (uint32_t)ti) >= thr;
     const uint32_t mh = __ballot_sync(0xffffffffu, hp), mt = __ballot_sync(0xffffffffu, tp);
-    if (hp) ms.scal[__popc(mh & lanemask_lt())] = comp_key(hx, (uint32_t)hi_i);
-    if (tp) ms.scal[__popc(mh) + __popc(mt & lanemask_lt())] = comp_key(tx, (uint32_t)ti);
+    if (hp) ms.scal[__popc(mh & lanemask_lt())] = comp_key(hx, pos0 + (uint32_t)hi_i);
+    if (tp) ms.scal[__popc(mh) + __popc(mt & lanemask_lt())] = comp_key(tx, pos0 + (uint32_t)ti);
     if (lane == 0) ms.nscal = __popc(mh) + __popc(mt);
   };
 
@@ -266,7 +273,7 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
     }
     const float x = to_f32(celem[i]);
     const uint32_t pos = (uint32_t)(a0 + cidx[i / EPV] * EPV + (int32_t)(i % EPV));
-    key = comp_key(x, pos);
+    key = comp_key(x, pos0 + pos);
     return key >= thr && !pen_bit(pos);
   };
 
@@ -345,7 +352,7 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
       thr_f = te;
       thr = te == -INFINITY ? 0ull : ((uint64_t)f32_key(te) << 32);
     }
-    if (rank == 0 && warp == 0) head_tail(pass_no == 0);
+    if (own_scal && warp == 0) head_tail(pass_no == 0);
     // consume batches.  While the threshold is a plain value (low key bits
     // zero) "x >= thr_f" IS the exact admission test: one max + compare per
     // vector.  After an overflow cut it is a full composite key and the exact
@@ -378,7 +385,7 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
             bool ex = false;
 #pragma unroll
             for (int e = 0; e < EPV; ++e)
-              ex |= comp_key(vec_elem<T>(v[j], e), (uint32_t)(a0 + idx * EPV + e)) >= thr;
+              ex |= comp_key(vec_elem<T>(v[j], e), pos0 + (uint32_t)(a0 + idx * EPV + e)) >= thr;
             if (!ex) vm &= ~(1u << j);
           }
         }
@@ -417,12 +424,12 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
     }
     __syncthreads();
     const bool overflow = ms.overflow != 0u;
-    n_valid = count_valid(get_c, min(ms.cnt, ccap) * EPV + (rank == 0 ? ms.nscal : 0u));
+    n_valid = count_valid(get_c, min(ms.cnt, ccap) * EPV + (own_scal ? ms.nscal : 0u));
     bool again = false;
     if (overflow) {
       // the buffer holds a subset of the admitted elements: its kp-th largest
       // key is a valid, strictly higher threshold
-      const uint64_t t1 = block_select_threshold<NT>(get_c, ccap * EPV + (rank == 0 ? ms.nscal : 0u), n_valid,
+      const uint64_t t1 = block_select_threshold<NT>(get_c, ccap * EPV + (own_scal ? ms.nscal : 0u), n_valid,
                                                      kp, bhist, ms.bcast);
       if (t1 > thr) thr = t1;
       again = true;
@@ -444,7 +451,7 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
   lapk(18);
   // ---- CTA-level exact top-kp
   {
-    const uint32_t ns = min(ms.cnt, ccap) * EPV + (rank == 0 ? ms.nscal : 0u);
+    const uint32_t ns = min(ms.cnt, ccap) * EPV + (own_scal ? ms.nscal : 0u);
     const uint64_t t = block_select_threshold<NT>(get_c, ns, n_valid, kp, bhist, ms.bcast);
     for (uint32_t i = tid; i < ns; i += NT) {
       uint64_t kk;

@@ -8,6 +8,7 @@
 namespace dp {
 
 enum Mode : int { kFull = 0, kHot = 1, kTail = 2 };
+constexpr int kMaxShards = 8;
 
 struct SampleArgs {
   const void* logits;
@@ -40,6 +41,12 @@ struct SampleArgs {
   int32_t* fb_count;            //   appended here for the general kernel (NULL: none routed)
   int32_t force_general;        // the general kernel decides every listed row
   int32_t update_pen;           // record each decided token in the penalty state (fused K5)
+  // TP-sharded kFull rows (nshard > 0): vocab shard s = positions
+  // [s * shard_n, (s + 1) * shard_n) of row b at shard[s] + b * ld, read in
+  // place by cluster rank s of the top-k kernel (split == nshard)
+  const void* shard[kMaxShards];
+  int64_t shard_n;
+  int32_t nshard;
 };
 
 DP_DEV int64_t dom_lo(const SampleArgs& a, int mode) { return mode == kTail ? a.H : 0; }
@@ -58,6 +65,16 @@ DP_DEV float row_value(const SampleArgs& a, int row, int64_t pos) {
   if (a.tail_logits && pos >= a.H)
     return Elem<T>::get(reinterpret_cast<const T*>(a.tail_logits) + (int64_t)row * a.tail_ld, pos - a.H);
   return Elem<T>::get(reinterpret_cast<const T*>(a.logits) + (int64_t)row * a.ld, pos);
+}
+// raw logit at domain position q of a row whose domain starts at rowp
+// (TP-sharded kFull rows: the owning shard's element)
+template <typename T>
+DP_DEV float dom_value(const SampleArgs& a, int row, const T* rowp, int64_t q) {
+  if (a.nshard > 0) {
+    const int64_t s = q / a.shard_n;
+    return Elem<T>::get(reinterpret_cast<const T*>(a.shard[s]) + (int64_t)row * a.ld, q - s * a.shard_n);
+  }
+  return Elem<T>::get(rowp, q);
 }
 DP_DEV int32_t pos_to_id(const SampleArgs& a, int64_t pos) {
   return a.perm ? __ldg(a.perm + pos) : (int32_t)pos;

@@ -194,6 +194,49 @@ class DecisionPlane:
             raise ValueError(f"unknown variant {variant!r}")
         return d
 
+    def sample_sharded(self, shards, iteration: int, uniforms=None, update: bool = True, debug: bool = False,
+                       topk_stride: int = 0) -> Decisions:
+        """Full-vocabulary decisions over TP-sharded logits, read in place:
+        `shards` = t <= 8 CUDA tensors [B, V/t] (vocab [s V/t, (s+1) V/t) in
+        shard s), one row stride, unit stride along the vocabulary — the
+        AssembledLogitsView / assemble_view contract (transport.py:460-557) on
+        the device.  Same decisions as `sample` on the stitched rows.  The
+        shards are stitched (one device copy) only when some row has top-k off
+        or wider than the top-k kernel takes (dp_sample_full_sharded's
+        DP_ERR_UNSUPPORTED) or the shards do not share a row stride."""
+        import torch
+
+        t = len(shards)
+        if t < 1 or t > 8:
+            raise ValueError("need 1..8 vocab shards")
+        w = shards[0].shape[1] if shards[0].dim() == 2 else -1
+        for x in shards:
+            if x.dim() != 2 or x.shape[0] != self.batch or x.shape[1] != w:
+                raise ValueError(f"shard tiling broken: every shard must be [{self.batch}, V/t]")
+            if not x.is_cuda or x.stride(1) != 1 or x.dtype != shards[0].dtype:
+                raise ValueError("shards must be CUDA tensors of one dtype with unit stride along the vocabulary")
+        if w * t != self.vocab_size:
+            raise ValueError(f"shards cover {w * t} ids, vocabulary has {self.vocab_size}")
+        self.last_stitched = True   # read by the tests: which path decided the call
+        if any(x.stride(0) != shards[0].stride(0) for x in shards):
+            return self.sample(torch.cat(list(shards), dim=1), iteration, uniforms=uniforms, update=update,
+                               debug=debug, topk_stride=topk_stride)
+        dt = _dtype_code(shards[0])
+        d = self._outputs(debug, topk_stride)
+        dbg = self._debug_struct(d, topk_stride, debug)
+        self._plan.fuse_update = 1 if update else 0
+        ptrs = (C.c_void_p * t)(*[x.data_ptr() for x in shards])
+        st = N.load().dp_sample_full_sharded(
+            ptrs, t, dt, self.batch, self.vocab_size, shards[0].stride(0), _ptr(self._params_dev),
+            C.byref(self.state.native), _ptr(uniforms), _ptr(self._seq_dev), int(iteration), _ptr(d.token),
+            _ptr(d.logprob), _ptr(d.flags), C.byref(dbg), C.byref(self._plan), _stream())
+        if st == N.DP_ERR_UNSUPPORTED:
+            return self.sample(torch.cat(list(shards), dim=1), iteration, uniforms=uniforms, update=update,
+                               debug=debug, topk_stride=topk_stride)
+        N.check(st, "dp_sample_full_sharded")
+        self.last_stitched = False
+        return d
+
     def sample_split(self, hot, tail, iteration: int, summary, uniforms=None, update: bool = True,
                      debug: bool = False, topk_stride: int = 0, summary_raw: bool = False) -> Decisions:
         """SHVS over split storage: `hot` = [B, >=H] CUDA tensor with the hot

@@ -526,3 +526,68 @@ def test_shvs_bf16_rows_match_oracle(torch_cuda, storage):
             states[b].update(int(dec[b].token))
         plane.state.update(torch.from_numpy(np.array([dd.token for dd in dec], np.int32)).cuda())
     print("exemptions:", exempt)
+
+
+@pytest.mark.parametrize("t,v,bf16", [(2, 32768, False), (4, 50000, False), (8, 50000, True), (8, 128256, False)])
+def test_tp_sharded_rows_match_stitched_and_oracle(torch_cuda, t, v, bf16):
+    """TP-sharded ingestion (AssembledLogitsView, transport.py:460-557): t vocab
+    shards read in place by one cluster rank each must decide exactly as the
+    stitched rows (tokens, logprobs, flags, penalty state) and as the oracle.
+    V=50000 gives shard widths whose rows start 8 bytes off a 16-byte boundary
+    (scalar head / tail elements on every rank)."""
+    torch = torch_cuda
+    bsz = 24
+    kinds = [dict(temperature=0.8, top_k=1), dict(temperature=0.8, top_k=50),
+             dict(temperature=0.7, top_k=200, top_p=0.9, min_p=0.05),
+             dict(temperature=0.8, top_k=50, top_p=0.9, min_p=0.05, rep_penalty=1.1, presence_penalty=0.5,
+                  frequency_penalty=0.1)]
+    params = [O.Params(**kinds[b % len(kinds)], seed=b) for b in range(bsz)]
+    prompts = [np.random.default_rng(900 + b).integers(0, v, 24) for b in range(bsz)]
+    states = [O.State.new(p, v) for p in prompts]
+    src = O.Synthetic(v)
+    a = plane_for(torch, v, params, prompts)
+    b_ = plane_for(torch, v, params, prompts)
+    w = v // t
+    exempt = []
+    for it in range(3):
+        xw = torch.from_numpy(src.wire(it, range(bsz)))
+        if bf16:
+            xw = xw.bfloat16()
+        x = xw.float().numpy()
+        xd = xw.cuda()
+        shards = [xd[:, s * w:(s + 1) * w].contiguous() for s in range(t)]
+        ds = a.sample_sharded(shards, it)
+        assert a.last_stitched is False   # decided in place by dp_sample_full_sharded
+        dc = b_.sample(xd, it)
+        assert torch.equal(ds.token, dc.token) and torch.equal(ds.flags, dc.flags)
+        assert torch.equal(ds.logprob, dc.logprob)
+        for f in ("ids", "out_count", "len"):
+            assert torch.equal(getattr(a.state, f), getattr(b_.state, f)), f
+        dec = [O.sample_full_row(x[r], states[r], params[r], O.uniforms_per_row([params[r].seed], it, [r])[0])
+               for r in range(bsz)]
+        compare(f"tp{t}/V{v}/it{it}", ds.token.cpu().numpy(), ds.logprob.cpu().numpy(), dec, exempt, lp_tol=1e-6)
+        for r in range(bsz):
+            states[r].update(int(dec[r].token))
+    print("exemptions:", exempt)
+
+
+def test_tp_sharded_stitches_when_rows_need_other_kernels(torch_cuda):
+    """Rows with top-k off route outside the top-k kernel: sample_sharded
+    stitches the shards and still decides exactly as sample(); a tiling that
+    does not cover the vocabulary is refused (IncompleteIterationError's
+    condition, transport.py:474-489)."""
+    torch = torch_cuda
+    v, bsz, t = 32768, 8, 4
+    params = [O.Params(temperature=0.9, top_p=0.8, seed=b) if b % 2 else O.Params(temperature=0.9, top_k=20, seed=b)
+              for b in range(bsz)]
+    prompts = [np.random.default_rng(b).integers(0, v, 8) for b in range(bsz)]
+    a = plane_for(torch, v, params, prompts)
+    b_ = plane_for(torch, v, params, prompts)
+    xd = torch.from_numpy(O.Synthetic(v).wire(1, range(bsz))).cuda()
+    w = v // t
+    shards = [xd[:, s * w:(s + 1) * w].contiguous() for s in range(t)]
+    ds, dc = a.sample_sharded(shards, 1), b_.sample(xd, 1)
+    assert a.last_stitched is True
+    assert torch.equal(ds.token, dc.token) and torch.equal(ds.logprob, dc.logprob)
+    with pytest.raises(ValueError):
+        a.sample_sharded(shards[:-1], 2)
