@@ -176,7 +176,11 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
   // ---- segment geometry (32-bit vector indices: V < 2^31)
   // TP-sharded rows: this CTA's segment is its own vocab shard, read in place
   // (positions offset by pos0); otherwise a vector-aligned chunk of the row
+#ifdef DP_NO_SHARD
+  constexpr bool sharded = false;   // A/B build knob
+#else
   const bool sharded = MODE == kFull && a.nshard > 0;
+#endif
   const T* segp = sharded ? reinterpret_cast<const T*>(a.shard[rank]) + (int64_t)row * a.ld : rowp;
   const int64_t n_seg = sharded ? a.shard_n : n;
   const uint32_t pos0 = sharded ? rank * (uint32_t)a.shard_n : 0u;
