@@ -151,7 +151,7 @@ DP_API int dp_sample_full(const void* logits, int dtype, int64_t B, int64_t V, i
  * shards[s] + b * ld elements (ld >= W; the reference's (W, B) Fortran-order
  * LogitsShardBlock.values, core.py:185-201, is exactly this layout).
  * shards is a HOST array of t <= 8 device pointers (peer memory of other TP
- * ranks works once peer access is enabled).  One cluster of t CTAs decides a
+ * ranks is addressable once peer access is enabled; untested on >1 GPU).  One cluster of t CTAs decides a
  * row, CTA s streaming shard s; results equal dp_sample_full on the stitched
  * rows.  Rows must all carry top-k: plan->min_top_k > 0 and plan->max_top_k
  * within the top-k kernel's capacity, else DP_ERR_UNSUPPORTED (stitch and
