@@ -65,6 +65,29 @@ def test_library_rejects_bad_arguments_without_gpu(lib):
     assert st == N.DP_ERR_UNSUPPORTED
 
 
+def test_sharded_entry_checks_tiling_without_gpu(lib):
+    """dp_sample_full_sharded refuses what AssembledLogitsView refuses
+    (transport.py:474-489: unequal widths / broken tiling), before any CUDA call."""
+    import ctypes as C
+
+    from paper_2512_00719_b200 import _native as N
+
+    one = C.c_void_p(1)
+    pen = N.Penalty(1, 1, 1, 1, 4, 12)
+
+    def call(ptrs, t, v, ld):
+        arr = (C.c_void_p * max(len(ptrs), 1))(*ptrs)
+        return lib.dp_sample_full_sharded(arr, t, 0, 1, v, ld, one, C.byref(pen), None, one, 0, one, one, one,
+                                          None, None, None)
+
+    assert call([1, 1], 2, 13, 7) == N.DP_ERR_ARG and b"tile" in lib.dp_last_error()    # 13 % 2 != 0
+    assert call([1, 1], 2, 12, 5) == N.DP_ERR_ARG                                        # ld < V / t
+    assert call([1] * 9, 9, 18, 2) == N.DP_ERR_ARG and b"shard count" in lib.dp_last_error()
+    assert call([1, 0], 2, 12, 6) == N.DP_ERR_ARG and b"null shard" in lib.dp_last_error()
+    # valid tiling but no plan bounds: rows may lack top-k -> the caller stitches
+    assert call([1, 1], 2, 12, 6) == N.DP_ERR_UNSUPPORTED and b"stitch" in lib.dp_last_error()
+
+
 def test_product_package_never_imports_oracle():
     pkg = os.path.join(ROOT, "paper_2512_00719_b200")
     for dirpath, _, files in os.walk(pkg):
