@@ -294,7 +294,16 @@ int dp_sample_full_sharded(const void* const* shards, int32_t t, int dtype, int6
   a.flags = flags;
   if (debug_host) a.dbg = *debug_host;
   plan_topk(a, plan_host, B, V, dtype == DP_F32 ? 4 : 2);
-  a.split = t;   // cluster rank s streams shard s in place
+  // one t-CTA cluster per row while the batch leaves SMs idle; otherwise the
+  // fewest CTAs per row that stream <= 4 shards each (a cluster rank's select
+  // + push is the per-CTA overhead)
+  int32_t c = t;
+  if (B >= (int64_t)sm_count()) {
+    c = 1;
+    while (t / c > 4 || t % c != 0) ++c;
+  }
+  a.split = c;   // cluster rank r streams shards [r t/c, (r+1) t/c) in place
+  a.shard_per_cta = t / c;
   a.nshard = t;
   a.shard_n = V / t;
   for (int32_t s = 0; s < t; ++s) a.shard[s] = shards[s];

@@ -54,7 +54,7 @@ struct TopkSmem {
   uint32_t nl;
   uint32_t nscal;
   uint32_t tmp;
-  uint64_t scal[32];          // CTA 0: scalar head/tail candidates
+  uint64_t scal[64];          // scalar head/tail candidates (CTA 0; every rank of a sharded row, <= 4 shards)
   FinishScratch fin;
 };
 
@@ -90,7 +90,9 @@ __host__ __device__ inline TopkLayout topk_layout(int ccap, int kcap, int lcap, 
 #endif
 constexpr int kPrefetch = DP_PREFETCH;   // L2 prefetch distance, in batches
 
-template <typename T, int MODE, int NT, int U, bool NUC>
+// SH: TP-sharded kFull rows (a.nshard > 0), a separate instantiation so the
+// contiguous-row code keeps its single-segment stream
+template <typename T, int MODE, int NT, int U, bool NUC, bool SH>
 __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample_kernel(SampleArgs a) {
   constexpr int NW = NT / 32;
   constexpr int EPV = Elem<T>::kPerVec;
@@ -176,25 +178,36 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
   // ---- segment geometry (32-bit vector indices: V < 2^31)
   // TP-sharded rows: this CTA's segment is its own vocab shard, read in place
   // (positions offset by pos0); otherwise a vector-aligned chunk of the row
-#ifdef DP_NO_SHARD
-  constexpr bool sharded = false;   // A/B build knob
-#else
-  const bool sharded = MODE == kFull && a.nshard > 0;
-#endif
-  const T* segp = sharded ? reinterpret_cast<const T*>(a.shard[rank]) + (int64_t)row * a.ld : rowp;
-  const int64_t n_seg = sharded ? a.shard_n : n;
-  const uint32_t pos0 = sharded ? rank * (uint32_t)a.shard_n : 0u;
+  constexpr bool sharded = SH && MODE == kFull;
+  // a sharded row's CTA streams shards [rank * spc, (rank + 1) * spc), one
+  // segment after another (set_segment)
+  const int spc = sharded ? a.shard_per_cta : 1;   // 1 at compile time unless SH
   const bool own_scal = rank == 0 || sharded;   // this CTA holds scalar head / tail elements
-  const uintptr_t addr = reinterpret_cast<uintptr_t>(segp);
-  const int32_t a0 = (int32_t)min64(n_seg, (int64_t)(((16u - (addr & 15u)) & 15u) / sizeof(T)));
-  const int32_t nvec = (int32_t)((n_seg - a0) / EPV);
-  const int32_t tail0 = a0 + nvec * EPV;
-  const int32_t chunk = sharded ? nvec : ((nvec + (int32_t)split - 1) / (int32_t)split + 31) & ~31;
-  const int32_t v_lo = sharded ? 0 : min(nvec, (int32_t)rank * chunk);
-  const int32_t v_hi = min(nvec, v_lo + chunk);
-  const uint4* vp = reinterpret_cast<const uint4*>(segp + a0);
+  const T* segp = rowp;
+  int64_t n_seg = n;
+  uint32_t pos0 = 0u;
+  int32_t a0 = 0, nvec = 0, tail0 = 0, v_lo = 0, v_hi = 0;
+  const uint4* vp = nullptr;
+  auto set_segment = [&](int g) {
+    if (sharded) {
+      const int s = (int)rank * spc + g;
+      segp = reinterpret_cast<const T*>(a.shard[s]) + (int64_t)row * a.ld;
+      n_seg = a.shard_n;
+      pos0 = (uint32_t)s * (uint32_t)a.shard_n;
+    }
+    const uintptr_t addr = reinterpret_cast<uintptr_t>(segp);
+    a0 = (int32_t)min64(n_seg, (int64_t)(((16u - (addr & 15u)) & 15u) / sizeof(T)));
+    nvec = (int32_t)((n_seg - a0) / EPV);
+    tail0 = a0 + nvec * EPV;
+    const int32_t chunk = sharded ? nvec : ((nvec + (int32_t)split - 1) / (int32_t)split + 31) & ~31;
+    v_lo = sharded ? 0 : min(nvec, (int32_t)rank * chunk);
+    v_hi = min(nvec, v_lo + chunk);
+    vp = reinterpret_cast<const uint4*>(segp + a0);
+  };
+  set_segment(0);
+  const int64_t seg_elems = sharded ? (int64_t)spc * a.shard_n : (int64_t)(v_hi - v_lo) * EPV;
   uint4* cvec = reinterpret_cast<uint4*>(cand);                 // admitted vectors
-  int32_t* cidx = reinterpret_cast<int32_t*>(cvec + ccap);      // their vector index
+  int32_t* cidx = reinterpret_cast<int32_t*>(cvec + ccap);      // their first element's row position
   const T* celem = reinterpret_cast<const T*>(cvec);
   auto pen_bit = [&](int64_t pos) -> bool {
     return MODE == kHot && ((bitmap[pos >> 5] >> (pos & 31)) & 1u);
@@ -252,6 +265,7 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
     return r;
   };
   // scalar head / tail elements (at most 2*EPV-2) belong to CTA 0 (warp 0)
+  uint32_t nscal_acc = 0u;   // warp 0: scalar keys appended so far this pass
   auto head_tail = [&](bool first) {
     const int32_t hi_i = lane, ti = tail0 + lane;
     const bool hv = hi_i < a0, tv = ti < n_seg;
@@ -262,9 +276,10 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
     const bool hp = hv && !pen_bit(hi_i) && comp_key(hx, pos0 + (uint32_t)hi_i) >= thr;
     const bool tp = tv && !pen_bit(ti) && comp_key(tx, pos0 + (uint32_t)ti) >= thr;
     const uint32_t mh = __ballot_sync(0xffffffffu, hp), mt = __ballot_sync(0xffffffffu, tp);
-    if (hp) ms.scal[__popc(mh & lanemask_lt())] = comp_key(hx, pos0 + (uint32_t)hi_i);
-    if (tp) ms.scal[__popc(mh) + __popc(mt & lanemask_lt())] = comp_key(tx, pos0 + (uint32_t)ti);
-    if (lane == 0) ms.nscal = __popc(mh) + __popc(mt);
+    if (hp) ms.scal[nscal_acc + __popc(mh & lanemask_lt())] = comp_key(hx, pos0 + (uint32_t)hi_i);
+    if (tp) ms.scal[nscal_acc + __popc(mh) + __popc(mt & lanemask_lt())] = comp_key(tx, pos0 + (uint32_t)ti);
+    nscal_acc += (uint32_t)(__popc(mh) + __popc(mt));
+    if (lane == 0) ms.nscal = nscal_acc;
   };
 
   // candidate source for the exact selection: elements of admitted vectors
@@ -276,8 +291,8 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
       return true;
     }
     const float x = to_f32(celem[i]);
-    const uint32_t pos = (uint32_t)(a0 + cidx[i / EPV] * EPV + (int32_t)(i % EPV));
-    key = comp_key(x, pos0 + pos);
+    const uint32_t pos = (uint32_t)cidx[i / EPV] + i % EPV;
+    key = comp_key(x, pos);
     return key >= thr && !pen_bit(pos);
   };
 
@@ -292,9 +307,11 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
   // element >= threshold (one aggregated atomic per lane per batch).
   float t_lb = -INFINITY;
   uint32_t n_valid = 0;
-  const int32_t base0 = v_lo + (int32_t)warp * 32 * U;
   for (int pass_no = 0;; ++pass_no) {
-    int32_t base = base0;
+  nscal_acc = 0u;
+  for (int g = 0; g < spc; ++g) {
+    if (g > 0 || (sharded && pass_no > 0)) set_segment(g);
+    int32_t base = v_lo + (int32_t)warp * 32 * U;
     if (lane == 0) {   // the first kPrefetch chunks after the first batch -> L2
 #pragma unroll
       for (int d = 1; d <= kPrefetch; ++d)
@@ -306,7 +323,7 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
       const int32_t idx = base + j * 32 + (int32_t)lane;
       v[j] = idx < v_hi ? ld_stream16(vp + idx) : neg_inf_vec<T>();
     }
-    if (pass_no == 0) {
+    if (pass_no == 0 && g == 0) {
       float mx = -INFINITY;
 #pragma unroll
       for (int j = 0; j < U; ++j) {
@@ -318,7 +335,7 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
         }
       }
       const uint32_t kw = (kp + NW - 1) / NW;
-      const float seg = (float)max(1, (v_hi - v_lo) * EPV);
+      const float seg = (float)max((int64_t)1, seg_elems);
       int rw = (int)ceilf(2.0f * (float)kp * (float)(32 * U * EPV) / seg);
       rw = max(1, min(32, rw));
       const uint32_t sorted = warp_sort_desc(f32_key(mx));
@@ -401,7 +418,7 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
           if ((vm >> j) & 1u) {
             if (slot < ccap) {
               cvec[slot] = v[j];
-              cidx[slot] = base + j * 32 + (int32_t)lane;
+              cidx[slot] = (int32_t)(pos0 + (uint32_t)(a0 + (base + j * 32 + (int32_t)lane) * EPV));
             } else {
               ms.overflow = 1u;
             }
@@ -426,6 +443,7 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
         }
       }
     }
+  }   // shards of this CTA
     __syncthreads();
     const bool overflow = ms.overflow != 0u;
     n_valid = count_valid(get_c, min(ms.cnt, ccap) * EPV + (own_scal ? ms.nscal : 0u));
@@ -538,7 +556,7 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
 // ---------------------------------------------------------------------------
 // host launcher
 
-template <typename T, int MODE, bool NUC>
+template <typename T, int MODE, bool NUC, bool SH = false>
 static cudaError_t launch_topk_t(const SampleArgs& a, int grid_rows, cudaStream_t st) {
 #ifndef DP_TOPK_NT
 #define DP_TOPK_NT 256
@@ -548,7 +566,7 @@ static cudaError_t launch_topk_t(const SampleArgs& a, int grid_rows, cudaStream_
   const int64_t n = MODE == kFull ? a.V : (MODE == kHot ? a.H : a.V - a.H);
   const int bm_words = MODE == kHot ? (int)((n + 31) / 32) + 1 : 0;
   const TopkLayout L = topk_layout<NT>(a.wcap, a.kcap, a.lcap, bm_words, a.split);
-  auto kern = topk_sample_kernel<T, MODE, NT, U, NUC>;
+  auto kern = topk_sample_kernel<T, MODE, NT, U, NUC, SH>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
@@ -568,6 +586,7 @@ static cudaError_t launch_topk_t(const SampleArgs& a, int grid_rows, cudaStream_
 
 template <typename T, bool NUC>
 static cudaError_t launch_topk_m(const SampleArgs& a, int mode, int grid_rows, cudaStream_t st) {
+  if (mode == kFull && a.nshard > 0) return launch_topk_t<T, kFull, false, true>(a, grid_rows, st);
   if (mode == kFull) return launch_topk_t<T, kFull, NUC>(a, grid_rows, st);
   if (mode == kHot) return launch_topk_t<T, kHot, NUC>(a, grid_rows, st);
   return launch_topk_t<T, kTail, NUC>(a, grid_rows, st);

@@ -47,6 +47,7 @@ struct SampleArgs {
   const void* shard[kMaxShards];
   int64_t shard_n;
   int32_t nshard;
+  int32_t shard_per_cta;        // shards one CTA streams (nshard = split * shard_per_cta)
 };
 
 DP_DEV int64_t dom_lo(const SampleArgs& a, int mode) { return mode == kTail ? a.H : 0; }
