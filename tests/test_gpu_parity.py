@@ -591,3 +591,47 @@ def test_tp_sharded_stitches_when_rows_need_other_kernels(torch_cuda):
     assert torch.equal(ds.token, dc.token) and torch.equal(ds.logprob, dc.logprob)
     with pytest.raises(ValueError):
         a.sample_sharded(shards[:-1], 2)
+
+
+@pytest.mark.parametrize("t,bf16", [(2, False), (4, True), (6, False), (8, False)])
+def test_tp_sharded_multi_shard_ctas_match_stitched(torch_cuda, t, bf16):
+    """B >= #SMs: one CTA streams several shards in turn (t/c per CTA, c-CTA
+    clusters).  Decisions, logprobs, flags and penalty state are identical to
+    the stitched rows; a row sample is checked against the oracle."""
+    torch = torch_cuda
+    v, bsz = 50016, 160          # 50016 / 6 = 8336, / 8 = 6252: misaligned shard rows
+    kinds = [dict(temperature=0.8, top_k=1), dict(temperature=0.8, top_k=50),
+             dict(temperature=0.8, top_k=50, top_p=0.9, min_p=0.05, rep_penalty=1.1, presence_penalty=0.5,
+                  frequency_penalty=0.1)]
+    params = [O.Params(**kinds[b % len(kinds)], seed=b) for b in range(bsz)]
+    prompts = [np.random.default_rng(1300 + b).integers(0, v, 16) for b in range(bsz)]
+    a = plane_for(torch, v, params, prompts)
+    b_ = plane_for(torch, v, params, prompts)
+    src = O.Synthetic(v)
+    w = v // t
+    for it in range(2):
+        xw = torch.from_numpy(src.wire(it, range(bsz)))
+        if bf16:
+            xw = xw.bfloat16()
+        xd = xw.cuda()
+        shards = [xd[:, s * w:(s + 1) * w].contiguous() for s in range(t)]
+        ds = a.sample_sharded(shards, it)
+        assert a.last_stitched is False
+        dc = b_.sample(xd, it)
+        assert torch.equal(ds.token, dc.token) and torch.equal(ds.flags, dc.flags)
+        assert torch.equal(ds.logprob, dc.logprob)
+        for f in ("ids", "out_count", "len"):
+            assert torch.equal(getattr(a.state, f), getattr(b_.state, f)), f
+    # oracle on a row sample of the first iteration (fresh states)
+    c = plane_for(torch, v, params, prompts)
+    xw = torch.from_numpy(src.wire(0, range(bsz)))
+    if bf16:
+        xw = xw.bfloat16()
+    x = xw.float().numpy()
+    xd = xw.cuda()
+    d = c.sample_sharded([xd[:, s * w:(s + 1) * w].contiguous() for s in range(t)], 0)
+    rows = list(range(0, bsz, 9))
+    dec = [O.sample_full_row(x[r], O.State.new(prompts[r], v), params[r],
+                             O.uniforms_per_row([params[r].seed], 0, [r])[0]) for r in rows]
+    exempt = []
+    compare(f"tp{t}-multi", d.token.cpu().numpy()[rows], d.logprob.cpu().numpy()[rows], dec, exempt, lp_tol=1e-6)
