@@ -36,5 +36,17 @@ for it in range(2):
     plane_s.sample_split(xs[:, :2048].contiguous(), xs[:, 2048:].contiguous(), 10 + it, summ, summary_raw=True)
 plane_k = DecisionPlane(v, params, prompts=prompts, max_generated=16, kernel=2, hot=hot)
 plane_k.sample(xs, 3, variant="shvs", summary=summ, summary_raw=True)
+# TP-sharded rows: one shard per cluster rank (B < #SMs) and several shards
+# per CTA (B >= #SMs), misaligned shard rows
+for bt, t in ((12, 4), (160, 8)):
+    vt = 8200
+    pt = [SamplingParams(**kinds[i % 2 if i % 2 == 0 else 3], seed=i) for i in range(bt)]
+    pr = [np.random.default_rng(i).integers(0, vt, 8) for i in range(bt)]
+    plane_t = DecisionPlane(vt, pt, prompts=pr, max_generated=16)
+    xt = SyntheticSource(vt, device="cuda").generate(0, range(bt))
+    w = vt // t
+    for it in range(2):
+        plane_t.sample_sharded([xt[:, s * w:(s + 1) * w].contiguous() for s in range(t)], it)
+        assert plane_t.last_stitched is False
 torch.cuda.synchronize()
 print("sanitize workload done")
