@@ -504,9 +504,17 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
       }
       __syncthreads();
       if (tid == 0) mbar_remote_arrive(dsmem_addr(&ms.mbar, 0));
-      // nothing of this CTA is read remotely: without a next row it retires
-      // now and frees its slot while CTA 0 finishes the row
-      if (ridx + (int)(gridDim.x / split) >= nrows) return;
+      // without a next row: leave (after the cluster's final barrier)
+      if (ridx + (int)(gridDim.x / split) >= nrows) {
+#ifndef DP_CLUSTER_EARLY_RETIRE
+        // every rank leaves together: no rank exits while a peer may still
+        // address the cluster's shared memory (compute-sanitizer racecheck
+        // clean; retiring right after the push is the opt-in
+        // DP_CLUSTER_EARLY_RETIRE build, ~1% faster SHVS tail)
+        cluster_sync();
+#endif
+        return;
+      }
       cluster_sync();   // end of row: CTA 0 is done with the receive buffers
       phase ^= 1u;
       continue;
@@ -544,7 +552,12 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
                                  tid, [] { __syncthreads(); }, nullptr, mtau_hi);
   }
   if (split > 1) {
-    if (ridx + (int)(gridDim.x / split) >= nrows) return;   // the peers retired after their push
+    if (ridx + (int)(gridDim.x / split) >= nrows) {   // last row: the cluster's final barrier, then exit
+#ifndef DP_CLUSTER_EARLY_RETIRE
+      cluster_sync();
+#endif
+      return;
+    }
     cluster_sync();   // end of row: the receive buffers may be rewritten
     phase ^= 1u;
   } else {
