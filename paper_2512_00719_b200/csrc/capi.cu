@@ -295,12 +295,14 @@ int dp_sample_full_sharded(const void* const* shards, int32_t t, int dtype, int6
   if (debug_host) a.dbg = *debug_host;
   plan_topk(a, plan_host, B, V, dtype == DP_F32 ? 4 : 2);
   // one t-CTA cluster per row while the batch leaves SMs idle; otherwise the
-  // fewest CTAs per row that stream <= 4 shards each (a cluster rank's select
-  // + push is the per-CTA overhead)
+  // fewest CTAs per row (a cluster rank's select + push is the per-CTA
+  // overhead).  A CTA keeps <= 2 (EPV - 1) scalar head / tail keys per shard
+  // in 64 slots: <= 8 fp32 shards, <= 4 bf16 shards
+  const int32_t max_spc = dtype == DP_F32 ? 8 : 4;
   int32_t c = t;
   if (B >= (int64_t)sm_count()) {
     c = 1;
-    while (t / c > 4 || t % c != 0) ++c;
+    while (t / c > max_spc || t % c != 0) ++c;
   }
   a.split = c;   // cluster rank r streams shards [r t/c, (r+1) t/c) in place
   a.shard_per_cta = t / c;

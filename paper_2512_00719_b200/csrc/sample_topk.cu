@@ -54,7 +54,7 @@ struct TopkSmem {
   uint32_t nl;
   uint32_t nscal;
   uint32_t tmp;
-  uint64_t scal[64];          // scalar head/tail candidates (CTA 0; every rank of a sharded row, <= 4 shards)
+  uint64_t scal[64];          // scalar head/tail candidates (CTA 0; every rank of a sharded row: <= 8 fp32 / 4 bf16 shards)
   FinishScratch fin;
 };
 
