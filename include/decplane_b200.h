@@ -46,6 +46,7 @@ typedef enum {
 typedef enum { DP_F32 = 0, DP_BF16 = 1 } dp_dtype_t;
 
 /* per-row flag bits */
+#define DP_FLAG_EOS            0x01u  /* the token is an end-of-sequence id (TokenDecision.is_eos) */
 #define DP_FLAG_ACCEPTED_HOT   0x02u  /* SHVS took the hot path (TokenDecision.accepted_hot) */
 #define DP_FLAG_NEAR_BOUNDARY  0x04u  /* a draw / accept / top-p / min-p decision was within
                                          1e-6 of its flip point (logged by the host)          */
@@ -77,6 +78,10 @@ typedef struct {
   int32_t* prompt_len;
   int32_t  cap;
   int32_t  vocab_size;
+  int32_t  max_len;     /* host-known upper bound of len[b] over the call's rows
+                           (prompt uniques + tokens recorded since the last reset);
+                           0 = unknown (cap).  Sizes the kernels' candidate lists. */
+  int32_t  reserved;
 } dp_penalty_t;
 
 /* Optional per-row diagnostics (any field may be NULL). */
@@ -90,7 +95,8 @@ typedef struct {
   double*  alpha;        /* [B] SHVS hot mass alpha (shvs.py:148-154)                      */
   uint64_t* bytes_touched; /* [B] logits bytes streamed for the row (VisitCounter analogue) */
   int64_t* stats;          /* [24] launch counters: 0 rows, 1 re-streams (estimate too high),
-                              2 re-streams (buffer overflow), 3 candidates admitted        */
+                              2 SHVS accept tests re-summed exactly (summary_raw),
+                              3 candidates admitted                                        */
 } dp_debug_t;
 
 /* Launch plan supplied by the host (nullable -> conservative defaults).
@@ -101,13 +107,22 @@ typedef struct {
  *   off).  When BOTH bounds are nonzero they are promises about every row of
  *   the call and kernels that no row can need are not launched; a row that
  *   breaks the promise is left undecided.  0 / 0 is always safe.
- * split: CTAs per row cluster for the streaming kernels (0 = auto, <= 8;
- *   -1 = the persistent warp-specialised TMA-ring kernel).
+ * split: CTAs per row cluster for the streaming kernels (0 = auto, <= 8).
  * kernel: 0 = auto, 1 = per-row CTA / cluster kernel, 2 = warp-per-row kernel
  *   for rows with top_k <= 64 (auto picks it for the SHVS hot pass at B >= SMs).
  * Rows with top-k off (top-p only, min-p only, neutral) are decided by the top-k
- *   kernel from their 512 largest values plus the domain mass when min_top_k == 0,
- *   with the general kernel as the exact fallback. */
+ *   kernel from their 256 largest values plus the domain mass when min_top_k == 0,
+ *   with the general kernel as the exact fallback.  That needs the workspace.
+ * workspace: CALLER-OWNED device scratch of workspace_len int32 elements
+ *   (>= dp_workspace_len(B)), used stream-ordered by the call only: the
+ *   library keeps no global buffers, so calls on different streams with
+ *   different workspaces never share state and CUDA-graph capture is safe.
+ *   NULL: nucleus rows take the (slower, exact) general kernel directly. */
+/* dp_plan_t.flags: test hook — every accept test of a raw-summary SHVS call
+ * goes through the exact re-sum (normally only the ones the cancelling
+ * correction cannot decide) */
+#define DP_PLAN_FORCE_RESUM 0x1
+
 typedef struct {
   int32_t max_top_k;
   int32_t split;
@@ -119,7 +134,9 @@ typedef struct {
   int32_t fuse_update;  /* record every decided token in the penalty state inside the
                            deciding kernel (update_output_histogram, penalty.py:18-32),
                            replacing a separate dp_penalty_update launch */
-  int32_t reserved;
+  int32_t flags;        /* DP_PLAN_* bits */
+  int32_t* workspace;   /* caller-owned scratch, see above (nullable) */
+  int64_t  workspace_len;
 } dp_plan_t;
 
 /* Library / device info. dp_device_check returns DP_OK when `device` is sm_100. */
@@ -127,6 +144,8 @@ DP_API int dp_version(void);
 DP_API int dp_device_check(int device);
 /* Human-readable reason of the last failing call on this thread. */
 DP_API const char* dp_last_error(void);
+/* int32 elements of dp_plan_t.workspace needed by a call over B rows. */
+DP_API int64_t dp_workspace_len(int64_t B);
 
 /* rng.pregenerate_slice (rng.py:94-113), keyed per row by params[b].seed:
  * out[b,0..2] = (u_hot, u_accept, u_tail) for (seed_b, iteration, seq_ids[b]). */
@@ -246,6 +265,13 @@ DP_API int dp_hot_mass_curve(const void* logits_hotfirst, int dtype, int64_t B, 
                       const dp_params_t* params, const dp_penalty_t* pen_host,
                       const int32_t* inv_perm, const int32_t* grid, int32_t n_grid,
                       double* out, void* stream);
+
+/* DecisionBatch wire payload (transport.py:173-184) for B decisions: out =
+ * u32 B, then per row u64 seq_id, u32 token, u8 flags (bit0 eos = DP_FLAG_EOS,
+ * bit1 accepted_hot, bit2 has_logprob = 1), f32 logprob; 4 + 17 B bytes,
+ * little-endian.  The host adds the 20-byte frame header and the CRC32. */
+DP_API int dp_encode_decisions(const int32_t* token, const double* logprob, const uint8_t* flags,
+                               const uint64_t* seq_ids, int64_t B, uint8_t* out, void* stream);
 
 /* Token-id all-gather across batch shards (DecisionLedger, transport.py:400-433):
  * ncclAllGather of int32 tokens over the communicator `nccl_comm` (an

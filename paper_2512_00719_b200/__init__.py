@@ -7,6 +7,7 @@ kernels behind the C ABI in include/decplane_b200.h.
 
 from .core import (
     DEFAULT_MAX_GENERATED,
+    LogitsShardBlock,
     TOP_K_DISABLED,
     DegenerateRowError,
     RangeError,
@@ -17,9 +18,11 @@ from .core import (
     validate_params,
 )
 from .penalty import PenaltyState, update_output_histogram
-from .sampler import VARIANT_FULL, VARIANT_SHVS, DecisionPlane, Decisions, sample_full, shvs_sample
+from .sampler import VARIANT_FULL, VARIANT_SHVS, DecisionPlane, Decisions
+from .service import (VARIANTS, ShvsRowContext, Sampler, _Sampler, make_shard_blocks, sample_full,
+                      shvs_sample)
 from .shvs import HotVocab, acceptance_rate, build_hot_vocab, load_hot_vocab_trace, save_hot_vocab_trace
-from .transport import partition_batch
+from .transport import AssembledLogitsView, DecisionBatch, assemble_view, partition_batch
 
 __version__ = "0.1.0"
 
@@ -28,5 +31,6 @@ __all__ = [
     "SequenceState", "TokenDecision", "new_sequence_state", "validate_params", "PenaltyState",
     "update_output_histogram", "VARIANT_FULL", "VARIANT_SHVS", "DecisionPlane", "Decisions", "sample_full",
     "shvs_sample", "HotVocab", "acceptance_rate", "build_hot_vocab", "load_hot_vocab_trace",
-    "save_hot_vocab_trace", "partition_batch", "__version__",
+    "save_hot_vocab_trace", "partition_batch", "__version__", "LogitsShardBlock", "VARIANTS", "ShvsRowContext",
+    "Sampler", "_Sampler", "make_shard_blocks", "AssembledLogitsView", "DecisionBatch", "assemble_view",
 ]

@@ -16,17 +16,19 @@ LIB_PATH = os.environ.get("DP_LIB") or os.path.join(_HERE, "_lib", "libdecplane_
 
 DP_OK, DP_ERR_ARG, DP_ERR_CUDA, DP_ERR_UNSUPPORTED, DP_ERR_CAPACITY = 0, -1, -2, -3, -4
 DP_F32, DP_BF16 = 0, 1
+FLAG_EOS = 0x01
 FLAG_ACCEPTED_HOT = 0x02
 FLAG_NEAR_BOUNDARY = 0x04
 FLAG_REJECTED = 0x08
 FLAG_PEN_OVERFLOW = 0x40
 FLAG_DEGENERATE = 0x80
+PLAN_FORCE_RESUM = 0x1
 
 EXPORTS = [
     "dp_version", "dp_device_check", "dp_last_error", "dp_uniforms", "dp_sample_full",
     "dp_row_summary", "dp_sample_shvs", "dp_penalty_update", "dp_penalty_reset",
     "dp_ready_rows", "dp_synth_logits", "dp_hot_mass_curve", "dp_row_summary_raw", "dp_sample_shvs_split",
-    "dp_stage_hot", "dp_sample_full_sharded",
+    "dp_stage_hot", "dp_sample_full_sharded", "dp_workspace_len", "dp_encode_decisions",
 ]
 
 
@@ -51,9 +53,12 @@ class Params(C.Structure):
 
 
 class Penalty(C.Structure):
+    """dp_penalty_t: the sparse device SequenceState table (core.py:100-169)."""
+
     _fields_ = [
         ("ids", C.c_void_p), ("out_count", C.c_void_p), ("len", C.c_void_p),
         ("prompt_len", C.c_void_p), ("cap", C.c_int32), ("vocab_size", C.c_int32),
+        ("max_len", C.c_int32), ("reserved", C.c_int32),
     ]
 
 
@@ -68,16 +73,21 @@ class Debug(C.Structure):
 class Plan(C.Structure):
     _fields_ = [("max_top_k", C.c_int32), ("split", C.c_int32), ("threads", C.c_int32),
                 ("summary_raw", C.c_int32), ("min_top_k", C.c_int32), ("kernel", C.c_int32),
-                ("fuse_update", C.c_int32), ("reserved", C.c_int32)]
+                ("fuse_update", C.c_int32), ("flags", C.c_int32),
+                ("workspace", C.c_void_p), ("workspace_len", C.c_int64)]
 
 
 assert C.sizeof(Params) == 64
+assert C.sizeof(Penalty) == 48
+assert C.sizeof(Plan) == 48
 
 _P, _I64, _U64, _I32, _D = C.c_void_p, C.c_int64, C.c_uint64, C.c_int32, C.c_double
 _SIGS = {
     "dp_version": ([], C.c_int),
     "dp_device_check": ([C.c_int], C.c_int),
     "dp_last_error": ([], C.c_char_p),
+    "dp_workspace_len": ([_I64], C.c_int64),
+    "dp_encode_decisions": ([_P, _P, _P, _P, _I64, _P, _P], C.c_int),
     "dp_uniforms": ([_P, _P, _I64, _U64, _P, _P], C.c_int),
     "dp_sample_full": ([_P, C.c_int, _I64, _I64, _I64, _P, C.POINTER(Penalty), _P, _P, _U64,
                         _P, _P, _P, C.POINTER(Debug), C.POINTER(Plan), _P], C.c_int),

@@ -114,9 +114,39 @@ __global__ void synth_kernel(const double* base, double noise, uint64_t seed, ui
   }
 }
 
+// DecisionBatch wire payload (transport.py:173-184): u32 count, then per row
+// u64 seq_id, u32 token_id, u8 flags (bit0 eos, bit1 accepted_hot,
+// bit2 has_logprob), f32 logprob — 17 unaligned little-endian bytes per row.
+__global__ void encode_decisions_kernel(const int32_t* token, const double* logprob, const uint8_t* flags,
+                                        const uint64_t* seq_ids, int64_t B, uint8_t* out) {
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b == 0) {
+    const uint32_t n = (uint32_t)B;
+    for (int i = 0; i < 4; ++i) out[i] = (uint8_t)(n >> (8 * i));
+  }
+  if (b >= B) return;
+  uint8_t* r = out + 4 + 17 * b;
+  const uint64_t s = seq_ids[b];
+  const uint32_t t = (uint32_t)token[b];
+  const uint8_t f = flags[b];
+  const uint8_t wf = (uint8_t)((f & DP_FLAG_EOS) | (f & DP_FLAG_ACCEPTED_HOT) | 0x04u);
+  const uint32_t lp = __float_as_uint((float)logprob[b]);
+  for (int i = 0; i < 8; ++i) r[i] = (uint8_t)(s >> (8 * i));
+  for (int i = 0; i < 4; ++i) r[8 + i] = (uint8_t)(t >> (8 * i));
+  r[12] = wf;
+  for (int i = 0; i < 4; ++i) r[13 + i] = (uint8_t)(lp >> (8 * i));
+}
+
 }  // namespace dp
 
 using namespace dp;
+
+cudaError_t dp_launch_encode(const int32_t* token, const double* logprob, const uint8_t* flags,
+                             const uint64_t* seq_ids, int64_t B, uint8_t* out, cudaStream_t st) {
+  encode_decisions_kernel<<<(unsigned)((B + 255) / 256 > 0 ? (B + 255) / 256 : 1), 256, 0, st>>>(token, logprob, flags,
+                                                                                               seq_ids, B, out);
+  return cudaGetLastError();
+}
 
 cudaError_t dp_launch_uniforms(const dp_params_t* params, const uint64_t* seq_ids, int64_t B,
                                uint64_t iteration, double* out, cudaStream_t st) {

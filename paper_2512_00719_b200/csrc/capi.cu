@@ -9,8 +9,9 @@
 namespace dp {
 cudaError_t launch_topk(const SampleArgs& a, int dtype, int mode, int grid_rows, cudaStream_t st);
 cudaError_t launch_general(const SampleArgs& a, int dtype, int mode, int grid_rows, cudaStream_t st);
+size_t topk_smem_bytes(const SampleArgs& a, int mode);
+cudaError_t launch_resum(const SampleArgs& a, int dtype, cudaStream_t st);
 cudaError_t launch_warp(const SampleArgs& a, int dtype, int mode, int grid_rows, cudaStream_t st);
-cudaError_t launch_stream(const SampleArgs& a, int dtype, int mode, int grid, int32_t* work, cudaStream_t st);
 cudaError_t launch_row_summary(const void* logits, int dtype, int64_t B, int64_t V, int64_t ld,
                                const dp_params_t* params, const dp_penalty_t& pen, const int32_t* inv_perm,
                                double* row_max, double* total, cudaStream_t st);
@@ -25,8 +26,15 @@ cudaError_t dp_launch_penalty_update(const dp_penalty_t&, const int32_t*, int64_
 cudaError_t dp_launch_penalty_reset(const dp_penalty_t&, int64_t, cudaStream_t);
 cudaError_t dp_launch_ready_rows(const void*, int, int64_t, int64_t, int64_t, const dp_params_t*,
                                  const dp_penalty_t&, double*, cudaStream_t);
+cudaError_t dp_launch_encode(const int32_t*, const double*, const uint8_t*, const uint64_t*, int64_t, uint8_t*,
+                             cudaStream_t);
 cudaError_t dp_launch_synth(const double*, double, uint64_t, uint64_t, const uint64_t*, int64_t, int64_t,
                             int64_t, const int32_t*, int, void*, cudaStream_t);
+
+// the ctypes mirrors (_native.py) and every caller rely on these layouts
+static_assert(sizeof(dp_params_t) == 64, "dp_params_t layout");
+static_assert(sizeof(dp_penalty_t) == 48, "dp_penalty_t layout");
+static_assert(sizeof(dp_plan_t) == 48, "dp_plan_t layout");
 
 namespace {
 
@@ -51,43 +59,33 @@ uint32_t pow2_at_least(uint32_t v) {
   while (p < v) p <<= 1;
   return p;
 }
-// per-device work counters of the persistent kernels (stream-ordered reuse;
-// concurrent calls on different streams of one device are not supported)
-int32_t* work_counter(int slot) {
-  static int32_t* g_work[64] = {nullptr};
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
-  if (!g_work[dev]) {
-    if (cudaMalloc(&g_work[dev], 16 * sizeof(int32_t)) != cudaSuccess) return nullptr;
-  }
-  return g_work[dev] + slot;
-}
-// Per-device fallback row lists for nucleus rows (slot 0: full, 1: SHVS hot,
-// 2: SHVS tail): [count, rows...], grown on demand.  Allocated by the first
-// (eager) call of a batch size; stream-ordered reuse like work_counter.
-int32_t* fallback_list(int slot, int64_t B) {
-  static int32_t* g_buf[64][3] = {{nullptr}};
-  static int64_t g_cap[64][3] = {{0}};
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
-  if (g_cap[dev][slot] < B + 1) {
-    int32_t* p = nullptr;
-    if (cudaMalloc(&p, (size_t)(B + 1) * sizeof(int32_t)) != cudaSuccess) return nullptr;
-    if (g_buf[dev][slot]) cudaFree(g_buf[dev][slot]);
-    g_buf[dev][slot] = p;
-    g_cap[dev][slot] = B + 1;
-  }
-  return g_buf[dev][slot];
-}
 // some row may have top-k off (the plan's lower bound does not exclude it)
 bool nucleus_possible(const dp_plan_t* plan) { return !(plan && plan->min_top_k > 0); }
-// arm the fallback list of a call (nucleus rows routed to the top-k kernel)
-cudaError_t arm_fallback(dp::SampleArgs& a, int slot, int64_t B, cudaStream_t st) {
-  int32_t* fb = fallback_list(slot, B);
-  if (!fb) return cudaErrorMemoryAllocation;
+// Caller-owned workspace (dp_plan_t.workspace, dp_workspace_len(B) int32
+// elements): three fallback row lists [count, rows...] of B + 1 entries
+// (slot 0: full path, 1: SHVS hot pass, 2: SHVS tail pass), the re-sum list
+// (slot 3) and B f64 hot masses (8-byte aligned).  Without a workspace
+// nucleus rows go straight to the general kernel (route_row).
+int64_t workspace_len(int64_t B) { return 4 * (B + 1) + 2 * B + 2; }
+int32_t* fallback_list(const dp_plan_t* plan, int slot, int64_t B) {
+  if (!plan || !plan->workspace || plan->workspace_len < workspace_len(B)) return nullptr;
+  return plan->workspace + slot * (B + 1);
+}
+double* resum_mass(const dp_plan_t* plan, int64_t B) {
+  int32_t* p = plan->workspace + 4 * (B + 1);
+  if ((reinterpret_cast<uintptr_t>(p) & 7u) != 0) ++p;
+  return reinterpret_cast<double*>(p);
+}
+// arm the fallback list of a call (nucleus rows routed to the top-k kernel);
+// false: no workspace, nucleus rows take the general kernel directly
+bool arm_fallback(dp::SampleArgs& a, const dp_plan_t* plan, int slot, int64_t B, cudaStream_t st, cudaError_t& e) {
+  int32_t* fb = fallback_list(plan, slot, B);
+  e = cudaSuccess;
+  if (!fb) return false;
   a.fb_count = fb;
   a.fb_rows = fb + 1;
-  return cudaMemsetAsync(fb, 0, sizeof(int32_t), st);
+  e = cudaMemsetAsync(fb, 0, sizeof(int32_t), st);
+  return true;
 }
 // the general kernel over the fallback list (after the top-k kernel)
 cudaError_t launch_fallback(const dp::SampleArgs& a, int dtype, int mode, int64_t B, cudaStream_t st) {
@@ -100,35 +98,20 @@ cudaError_t launch_fallback(const dp::SampleArgs& a, int dtype, int mode, int64_
   return dp::launch_general(g, dtype, mode, (int)B, st);
 }
 
-// the persistent TMA-ring kernel is opt-in (plan->split == -1) until it beats
-// the per-row CTA kernel; see sample_stream.cu
-bool use_stream(int64_t B, const dp_plan_t* plan) {
-  return plan && plan->split == -1 && B >= sm_count();
-}
-cudaError_t launch_sampler(const dp::SampleArgs& a, int dtype, int mode, int64_t B, bool stream, int slot,
-                           cudaStream_t st) {
-  if (stream) {
-    int32_t* w = work_counter(slot);
-    if (!w) return cudaErrorMemoryAllocation;
-    const int64_t grid = B < (int64_t)sm_count() ? B : (int64_t)sm_count();   // one persistent CTA per SM
-    return dp::launch_stream(a, dtype, mode, (int)grid, w, st);
-  }
-  return dp::launch_topk(a, dtype, mode, (int)B, st);
-}
 // Which kernels a call launches.  Every row is routed to exactly one kernel by
 // route_row (sampler.cuh); a kernel is skipped only when the plan's top-k
 // bounds (promises, see dp_plan_t) prove no row routes to it.
 struct Launches {
   bool warp, topk, general;
 };
-Launches plan_launches(dp::SampleArgs& a, const dp_plan_t* plan, int mode, int64_t B, int64_t n, bool persistent) {
+Launches plan_launches(dp::SampleArgs& a, const dp_plan_t* plan, int mode, int64_t B, int64_t n) {
   Launches L;
   const int kernel = plan ? plan->kernel : 0;
   const int64_t kmax = plan ? plan->max_top_k : 0, kmin = plan ? plan->min_top_k : 0;
   const bool bounded = kmax > 0 && kmin > 0 && kmax < n;
-  const int64_t cap = a.pen.cap;
+  const int64_t cap = dp::pen_bound(a.pen);
   a.use_warp = 0;
-  if (!persistent && mode != dp::kTail && kernel != 1) {
+  if (mode != dp::kTail && kernel != 1) {
     const bool auto_warp = mode == dp::kHot && B >= sm_count() && n <= 65536;
     a.use_warp = (kernel == 2 || auto_warp) ? 1 : 0;
   }
@@ -151,6 +134,20 @@ Launches plan_launches(dp::SampleArgs& a, const dp_plan_t* plan, int mode, int64
   return L;
 }
 
+// Shrink the top-k kernel's capacities until its shared memory fits one CTA
+// (final-list capacity first, then the admission buffer, then the selection).
+// Rows whose k + |list| no longer fit route to the general kernel (route_row).
+void fit_topk(dp::SampleArgs& a, int mode) {
+  int dev = 0, optin = 232448;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  while (dp::topk_smem_bytes(a, mode) > (size_t)optin) {
+    if (a.lcap > 256) a.lcap >>= 1;
+    else if (a.wcap > 1024) a.wcap >>= 1;
+    else if (a.kcap > 256) a.kcap >>= 1;
+    else break;
+  }
+}
+
 bool valid_pen(const dp_penalty_t* pen, int64_t V) {
   return pen && pen->ids && pen->out_count && pen->len && pen->cap >= 0 && pen->vocab_size == V;
 }
@@ -159,7 +156,7 @@ bool valid_pen(const dp_penalty_t* pen, int64_t V) {
 void plan_topk(dp::SampleArgs& a, const dp_plan_t* plan, int64_t B, int64_t n, int elem_bytes) {
   int32_t kmax = (plan && plan->max_top_k > 0) ? plan->max_top_k : 256;
   if (nucleus_possible(plan) && kmax < dp::kNucK) kmax = dp::kNucK;   // nucleus rows keep kNucK
-  const uint32_t kcap = pow2_at_least((uint32_t)kmax + (uint32_t)a.pen.cap);
+  const uint32_t kcap = pow2_at_least((uint32_t)kmax + (uint32_t)dp::pen_bound(a.pen));
   a.kcap = (int32_t)(kcap < 32u ? 32u : kcap);
   if (a.kcap > 2048) a.kcap = 2048;
   // vector slots of the streaming stage's candidate buffer (wcap field): the
@@ -167,7 +164,7 @@ void plan_topk(dp::SampleArgs& a, const dp_plan_t* plan, int64_t B, int64_t n, i
   // handled exactly (re-stream), so this only sizes the common case
   a.wcap = (int32_t)(4u * (uint32_t)a.kcap > 1024u ? 4u * (uint32_t)a.kcap : 1024u);
   if (a.wcap > 4096) a.wcap = 4096;
-  a.lcap = (int32_t)pow2_at_least((uint32_t)kmax + 2u * (uint32_t)a.pen.cap + 1u);
+  a.lcap = (int32_t)pow2_at_least((uint32_t)kmax + 2u * (uint32_t)dp::pen_bound(a.pen) + 1u);
   if (a.lcap > 4096) a.lcap = 4096;
   int split = plan && plan->split > 0 ? plan->split : 0;
   if (split == 0) {
@@ -196,6 +193,8 @@ extern "C" {
 int dp_version(void) { return 100; }
 
 const char* dp_last_error(void) { return g_err; }
+
+int64_t dp_workspace_len(int64_t B) { return B < 0 ? 0 : workspace_len(B); }
 
 int dp_device_check(int device) {
   cudaDeviceProp prop;
@@ -244,15 +243,14 @@ int dp_sample_full(const void* logits, int dtype, int64_t B, int64_t V, int64_t 
   a.flags = flags;
   if (debug_host) a.dbg = *debug_host;
   plan_topk(a, plan_host, B, V, dtype == DP_F32 ? 4 : 2);
-  const bool persistent = use_stream(B, plan_host);
-  if (persistent) a.split = 1;
+  fit_topk(a, dp::kFull);
   cudaError_t e = cudaSuccess;
-  const bool nuc = nucleus_possible(plan_host) && !persistent;
-  if (nuc && (e = arm_fallback(a, 0, B, st)) != cudaSuccess) return cuda_status(e, "dp_sample_full/fallback");
-  const Launches L = plan_launches(a, plan_host, dp::kFull, B, V, persistent);
+  const bool nuc = nucleus_possible(plan_host) && arm_fallback(a, plan_host, 0, B, st, e);
+  if (e != cudaSuccess) return cuda_status(e, "dp_sample_full/fallback");
+  const Launches L = plan_launches(a, plan_host, dp::kFull, B, V);
   if (L.warp && (e = dp::launch_warp(a, dtype, dp::kFull, (int)B, st)) != cudaSuccess)
     return cuda_status(e, "dp_sample_full/warp");
-  if (L.topk && (e = launch_sampler(a, dtype, dp::kFull, B, persistent, 0, st)) != cudaSuccess)
+  if (L.topk && (e = dp::launch_topk(a, dtype, dp::kFull, (int)B, st)) != cudaSuccess)
     return cuda_status(e, "dp_sample_full/topk");
   if (L.general && (e = dp::launch_general(a, dtype, dp::kFull, (int)B, st)) != cudaSuccess)
     return cuda_status(e, "dp_sample_full/general");
@@ -305,14 +303,15 @@ int dp_sample_full_sharded(const void* const* shards, int32_t t, int dtype, int6
     while (t / c > max_spc || t % c != 0) ++c;
   }
   a.split = c;   // cluster rank r streams shards [r t/c, (r+1) t/c) in place
+  fit_topk(a, dp::kFull);
   a.shard_per_cta = t / c;
   a.nshard = t;
   a.shard_n = V / t;
   for (int32_t s = 0; s < t; ++s) a.shard[s] = shards[s];
   // zero-copy only through the top-k kernel: every row must carry top-k
   // within the plan's bounds (the other kernels read contiguous rows)
-  const Launches L = plan_launches(a, plan_host, dp::kFull, B, V, false);
-  if (use_stream(B, plan_host) || L.warp || L.general || !L.topk)
+  const Launches L = plan_launches(a, plan_host, dp::kFull, B, V);
+  if (L.warp || L.general || !L.topk)
     return fail(DP_ERR_UNSUPPORTED,
                 "dp_sample_full_sharded: needs plan min_top_k > 0 and max_top_k within the top-k kernel's "
                 "capacity (stitch the shards and call dp_sample_full otherwise)%s");
@@ -405,43 +404,59 @@ int sample_shvs_impl(const void* logits, int dtype, int64_t B, int64_t V, int64_
   if (e != cudaSuccess) return cuda_status(e, "dp_sample_shvs/memset");
   a.reject_rows = rej_rows;
   a.reject_count = rej_count;
+  // raw producer summary: undecidable accept tests are re-summed exactly
+  const bool resum = plan_host && plan_host->summary_raw && H < V;
+  if (resum) {
+    int32_t* rl = fallback_list(plan_host, 3, B);
+    if (!rl) return fail(DP_ERR_ARG, "dp_sample_shvs: summary_raw needs the plan workspace (dp_workspace_len)%s");
+    a.resum_count = rl;
+    a.resum_rows = rl + 1;
+    a.resum_sh = resum_mass(plan_host, B);
+    a.force_resum = (plan_host->flags & DP_PLAN_FORCE_RESUM) ? 1 : 0;
+    if ((e = cudaMemsetAsync(rl, 0, sizeof(int32_t), st)) != cudaSuccess) return cuda_status(e, "dp_sample_shvs/memset");
+  }
   // hot pass over [0, H)
   plan_topk(a, plan_host, B, H, dtype == DP_F32 ? 4 : 2);
-  const bool persistent = use_stream(B, plan_host) && !tail_logits;
-  if (persistent) a.split = 1;
-  const bool nuc = nucleus_possible(plan_host) && !persistent;
-  if (nuc && (e = arm_fallback(a, 1, B, st)) != cudaSuccess) return cuda_status(e, "dp_sample_shvs/fallback");
-  const Launches L = plan_launches(a, plan_host, dp::kHot, B, H, persistent);
+  fit_topk(a, dp::kHot);
+  const bool nuc = nucleus_possible(plan_host) && arm_fallback(a, plan_host, 1, B, st, e);
+  if (e != cudaSuccess) return cuda_status(e, "dp_sample_shvs/fallback");
+  const Launches L = plan_launches(a, plan_host, dp::kHot, B, H);
   if (L.warp && (e = dp::launch_warp(a, dtype, dp::kHot, (int)B, st)) != cudaSuccess)
     return cuda_status(e, "dp_sample_shvs/hot-warp");
-  if (L.topk && (e = launch_sampler(a, dtype, dp::kHot, B, persistent, 1, st)) != cudaSuccess)
+  if (L.topk && (e = dp::launch_topk(a, dtype, dp::kHot, (int)B, st)) != cudaSuccess)
     return cuda_status(e, "dp_sample_shvs/hot-topk");
   if (L.general && (e = dp::launch_general(a, dtype, dp::kHot, (int)B, st)) != cudaSuccess)
     return cuda_status(e, "dp_sample_shvs/hot-general");
   if (nuc && (e = launch_fallback(a, dtype, dp::kHot, B, st)) != cudaSuccess)
     return cuda_status(e, "dp_sample_shvs/hot-fallback");
   if (H == V) return DP_OK;
+  if (resum && (e = dp::launch_resum(a, dtype, st)) != cudaSuccess) return cuda_status(e, "dp_sample_shvs/resum");
   // tail pass over [H, V) for the rows the hot pass rejected
   dp::SampleArgs t = a;
+  t.resum_rows = nullptr;
+  t.resum_count = nullptr;
   t.rows = rej_rows;
   t.row_count = rej_count;
   t.reject_rows = nullptr;
   t.reject_count = nullptr;
-  if (nuc && (e = arm_fallback(t, 2, B, st)) != cudaSuccess) return cuda_status(e, "dp_sample_shvs/fallback");
+  if (nuc) {
+    arm_fallback(t, plan_host, 2, B, st, e);
+    if (e != cudaSuccess) return cuda_status(e, "dp_sample_shvs/fallback");
+  }
   plan_topk(t, plan_host, B, V - H, dtype == DP_F32 ? 4 : 2);
   // The tail pass serves only the rejected rows (typically a few percent of
   // B, count known on the device only): 4-CTA clusters split each row over 4
   // SMs, and the clusters loop over the reject list, so a handful of
   // rejections costs one short row time rather than one long one.
   int64_t tail_clusters = B;
-  if (!persistent && !(plan_host && plan_host->split > 0)) {
+  if (!(plan_host && plan_host->split > 0)) {
     t.split = (V - H) >= 4 * 4096 ? 4 : 1;   // 4 measured best at C2 (2: 71, 4: 63, 8: 65 us per SHVS step)
     const int64_t slots = (int64_t)sm_count() * 2 / t.split;   // resident clusters (2 tail CTAs per SM)
     tail_clusters = B < slots ? B : slots;
   }
-  if (persistent) t.split = 1;
-  const Launches LT = plan_launches(t, plan_host, dp::kTail, B, V - H, persistent);
-  if (LT.topk && (e = launch_sampler(t, dtype, dp::kTail, tail_clusters, persistent, 2, st)) != cudaSuccess)
+  fit_topk(t, dp::kTail);
+  const Launches LT = plan_launches(t, plan_host, dp::kTail, B, V - H);
+  if (LT.topk && (e = dp::launch_topk(t, dtype, dp::kTail, (int)tail_clusters, st)) != cudaSuccess)
     return cuda_status(e, "dp_sample_shvs/tail-topk");
   if (LT.general && (e = dp::launch_general(t, dtype, dp::kTail, (int)B, st)) != cudaSuccess)
     return cuda_status(e, "dp_sample_shvs/tail-general");
@@ -522,6 +537,14 @@ int dp_synth_logits(const double* base_by_id, double noise, uint64_t seed, uint6
   return cuda_status(dp_launch_synth(base_by_id, noise, seed, iteration, seq_ids, B, V, ld, perm, dtype, out,
                                      (cudaStream_t)stream),
                      "dp_synth_logits");
+}
+
+int dp_encode_decisions(const int32_t* token, const double* logprob, const uint8_t* flags, const uint64_t* seq_ids,
+                        int64_t B, uint8_t* out, void* stream) {
+  if (!token || !logprob || !flags || !seq_ids || !out || B < 0)
+    return fail(DP_ERR_ARG, "dp_encode_decisions: null argument%s");
+  return cuda_status(dp_launch_encode(token, logprob, flags, seq_ids, B, out, (cudaStream_t)stream),
+                     "dp_encode_decisions");
 }
 
 int dp_hot_mass_curve(const void* logits, int dtype, int64_t B, int64_t V, int64_t ld, const double* row_max,

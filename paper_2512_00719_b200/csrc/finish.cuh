@@ -286,7 +286,7 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
 
   // kHot: alpha and the accept test first (shvs.py:223-236)
   double alpha = 1.0;
-  bool imprecise = false;
+  bool deferred = false;     // kHot: accept test left to the exact re-sum
   double s_dom = sh_unpen;   // nucleus: mass of the whole domain (see above)
   if (MODE == kHot) {
     double spen = 0.0;   // exact mass of penalized hot ids (f64)
@@ -315,20 +315,19 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
     s_dom = sH;
     const double S_prod = a.total_expsum[row];
     const double S = S_prod + corr;
-    // a raw summary dominated by since-penalized mass loses relative precision
-    imprecise = a.summary_raw && S_prod > 16.0 * S;
     const bool tail_empty = a.V == a.H;
     bool degenerate = false;
     if (!tail_empty) {
       if (!(S > 0.0) || !isfinite(S)) degenerate = true;
       else alpha = fmin(sH / S, 1.0);
     }
-    const bool accept = !degenerate && sH > 0.0 && (tail_empty || u[1] <= alpha);
+    deferred = sH > 0.0 && defer_accept(a, S_prod, S, alpha, u[1]);
+    const bool accept = deferred || (!degenerate && sH > 0.0 && (tail_empty || u[1] <= alpha));
     if (!accept) {
       if (t == 0) {
         uint8_t fl = DP_FLAG_REJECTED;
         if (degenerate || (tail_empty && !(sH > 0.0))) fl |= DP_FLAG_DEGENERATE;
-        else if (fabs(u[1] - alpha) < kBoundaryEps || imprecise) fl |= DP_FLAG_NEAR_BOUNDARY;
+        else if (fabs(u[1] - alpha) < kBoundaryEps) fl |= DP_FLAG_NEAR_BOUNDARY;
         a.flags[row] = fl;
         if (a.dbg.alpha) a.dbg.alpha[row] = alpha;
         if (a.dbg.margin) a.dbg.margin[row] = fabs(u[1] - alpha);
@@ -577,8 +576,8 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
       a.logprob[row] = d.logprob;
       uint8_t fl = MODE == kHot ? DP_FLAG_ACCEPTED_HOT : (MODE == kTail ? DP_FLAG_REJECTED : 0);
       double margin = d.margin;
-      if (MODE == kHot && a.V != a.H) margin = fmin(margin, fabs(u[1] - alpha));
-      if (margin < kBoundaryEps || imprecise) fl |= DP_FLAG_NEAR_BOUNDARY;
+      if (MODE == kHot && a.V != a.H && !deferred) margin = fmin(margin, fabs(u[1] - alpha));
+      if (margin < kBoundaryEps) fl |= DP_FLAG_NEAR_BOUNDARY;
       if (MODE == kTail) fl |= a.flags[row] & DP_FLAG_NEAR_BOUNDARY;
       a.flags[row] = fl;
       if (a.dbg.margin) a.dbg.margin[row] = MODE == kTail ? fmin(margin, a.dbg.margin[row]) : margin;
@@ -587,7 +586,8 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
       if (a.dbg.bytes_touched)
         a.dbg.bytes_touched[row] = (MODE == kTail ? a.dbg.bytes_touched[row] : 0ull) + (uint64_t)n * sizeof(T);
     }
-    if (!fb && !degen) warp_record_token(a, row, pos_to_id(a, (int64_t)fpos[d.index] + lo));   // fused K5
+    if (deferred && !fb && !degen && lane == 0) push_resum(a, row, s_dom);   // re-sum decides, then records
+    if (!fb && !degen && !deferred) warp_record_token(a, row, pos_to_id(a, (int64_t)fpos[d.index] + lo));   // fused K5
     if (a.dbg.topk_ids && !fb && !degen) {
       const int32_t m = min(k, a.dbg.topk_stride);
       for (int32_t j = lane; j < m; j += 32) {

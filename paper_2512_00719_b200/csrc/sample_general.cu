@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(kGenNT, 1) general_sample_kernel(SampleArgs a)
   PenEntry* pen = reinterpret_cast<PenEntry*>(smem + ((sizeof(GenSmem) + 15) & ~15));
   const int64_t n = dom_n(a, MODE);
   const int64_t lo = dom_lo(a, MODE);
-  uint32_t* bitmap = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(pen) + (size_t)a.pen.cap * sizeof(PenEntry));
+  uint32_t* bitmap = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(pen) + (size_t)pen_bound(a.pen) * sizeof(PenEntry));
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u;
   auto sync = [] { __syncthreads(); };
 
@@ -375,11 +375,11 @@ __global__ void __launch_bounds__(kGenNT, 1) general_sample_kernel(SampleArgs a)
 
   // kHot: alpha and the accept test (shvs.py:223-236); S_H relative to the
   // producer's row max m: S_H = W * exp(rmax - m)
-  double alpha = 1.0;
-  bool imprecise = false;
+  double alpha = 1.0, sH = 0.0;
+  bool deferred = false;   // accept test left to the exact re-sum (defer_accept)
   if (MODE == kHot) {
     const double mrow = a.row_max[row];
-    const double sH = ((double)W / kFix) * exp(rmax - mrow);
+    sH = ((double)W / kFix) * exp(rmax - mrow);
     double corr = 0.0;
     if (a.summary_raw) {
       corr = raw_summary_correction(a, row, p, plen_all, mrow, tid, kGenNT,
@@ -388,19 +388,19 @@ __global__ void __launch_bounds__(kGenNT, 1) general_sample_kernel(SampleArgs a)
     }
     const double S_prod = a.total_expsum[row];
     const double S = S_prod + corr;
-    imprecise = a.summary_raw && S_prod > 16.0 * S;
     const bool tail_empty = a.V == a.H;
     bool degenerate = false;
     if (!tail_empty) {
       if (!(S > 0.0) || !isfinite(S)) degenerate = true;
       else alpha = fmin(sH / S, 1.0);
     }
-    const bool accept = !degenerate && sH > 0.0 && (tail_empty || u[1] <= alpha);
+    deferred = sH > 0.0 && defer_accept(a, S_prod, S, alpha, u[1]);
+    const bool accept = deferred || (!degenerate && sH > 0.0 && (tail_empty || u[1] <= alpha));
     if (!accept) {
       if (tid == 0) {
         uint8_t fl = DP_FLAG_REJECTED;
         if (degenerate || (tail_empty && !(sH > 0.0))) fl |= DP_FLAG_DEGENERATE;
-        else if (fabs(u[1] - alpha) < kBoundaryEps || imprecise) fl |= DP_FLAG_NEAR_BOUNDARY;
+        else if (fabs(u[1] - alpha) < kBoundaryEps) fl |= DP_FLAG_NEAR_BOUNDARY;
         a.flags[row] = fl;
         if (a.dbg.alpha) a.dbg.alpha[row] = alpha;
         if (a.dbg.margin) a.dbg.margin[row] = fabs(u[1] - alpha);
@@ -659,8 +659,8 @@ __global__ void __launch_bounds__(kGenNT, 1) general_sample_kernel(SampleArgs a)
     a.token[row] = pos_to_id(a, gpos);
     a.logprob[row] = (r - rmax) - log((double)S_kept / kFix);
     uint8_t fl = MODE == kHot ? DP_FLAG_ACCEPTED_HOT : (MODE == kTail ? DP_FLAG_REJECTED : 0);
-    if (MODE == kHot && a.V != a.H) margin = fmin(margin, fabs(u[1] - alpha));
-    if (margin < kBoundaryEps || imprecise) fl |= DP_FLAG_NEAR_BOUNDARY;
+    if (MODE == kHot && a.V != a.H && !deferred) margin = fmin(margin, fabs(u[1] - alpha));
+    if (margin < kBoundaryEps) fl |= DP_FLAG_NEAR_BOUNDARY;
     if (MODE == kTail) fl |= a.flags[row] & DP_FLAG_NEAR_BOUNDARY;
     a.flags[row] = fl;
     if (a.dbg.margin) a.dbg.margin[row] = MODE == kTail ? fmin(margin, a.dbg.margin[row]) : margin;
@@ -668,7 +668,8 @@ __global__ void __launch_bounds__(kGenNT, 1) general_sample_kernel(SampleArgs a)
     if (MODE == kHot && a.dbg.alpha) a.dbg.alpha[row] = alpha;
     if (a.dbg.bytes_touched)
       a.dbg.bytes_touched[row] = (MODE == kTail ? a.dbg.bytes_touched[row] : 0ull) + (uint64_t)n * sizeof(T);
-    thread_record_token(a, row, pos_to_id(a, gpos));   // fused K5
+    if (deferred) push_resum(a, row, sH);   // the exact re-sum decides, then records
+    else thread_record_token(a, row, pos_to_id(a, gpos));   // fused K5
   }
   }
 }
@@ -676,7 +677,7 @@ __global__ void __launch_bounds__(kGenNT, 1) general_sample_kernel(SampleArgs a)
 template <typename T, int MODE>
 static cudaError_t launch_general_t(const SampleArgs& a, int grid_rows, cudaStream_t st) {
   const int64_t n = MODE == kFull ? a.V : (MODE == kHot ? a.H : a.V - a.H);
-  const size_t smem = ((sizeof(GenSmem) + 15) & ~15) + (size_t)a.pen.cap * sizeof(PenEntry) +
+  const size_t smem = ((sizeof(GenSmem) + 15) & ~15) + (size_t)pen_bound(a.pen) * sizeof(PenEntry) +
                       (size_t)((n + 31) / 32) * 4;
   auto kern = general_sample_kernel<T, MODE>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

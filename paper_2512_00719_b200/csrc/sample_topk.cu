@@ -605,6 +605,13 @@ static cudaError_t launch_topk_m(const SampleArgs& a, int mode, int grid_rows, c
   return launch_topk_t<T, kTail, NUC>(a, grid_rows, st);
 }
 
+// dynamic shared memory of a top-k launch with the call's capacities
+size_t topk_smem_bytes(const SampleArgs& a, int mode) {
+  const int64_t n = mode == kFull ? a.V : (mode == kHot ? a.H : a.V - a.H);
+  const int bm_words = mode == kHot ? (int)((n + 31) / 32) + 1 : 0;
+  return topk_layout<DP_TOPK_NT>(a.wcap, a.kcap, a.lcap, bm_words, a.split).total;
+}
+
 // 256 threads per CTA (the 128-thread variant measured slower at every
 // shape); the nucleus instantiation only when the call may hold such rows
 cudaError_t launch_topk(const SampleArgs& a, int dtype, int mode, int grid_rows, cudaStream_t st) {

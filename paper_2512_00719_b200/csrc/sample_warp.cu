@@ -431,8 +431,8 @@ __global__ void __launch_bounds__(kMW * 32, kMWBlocks) warp_sample_kernel(Sample
     // ---- decision inputs, evaluated by every thread (CTA-uniform)
     double u[3];
     get_uniforms(a, row, p, u);
-    double alpha = 1.0;
-    bool imprecise = false;
+    double alpha = 1.0, sH = 0.0;
+    bool deferred = false;   // accept test left to the exact re-sum (defer_accept)
     if (MODE == kHot) {   // alpha and the accept test (shvs.py:223-236)
       double sh_row = 0.0, spen = 0.0, sraw = 0.0, corr = 0.0;
 #pragma unroll
@@ -442,22 +442,22 @@ __global__ void __launch_bounds__(kMW * 32, kMWBlocks) warp_sample_kernel(Sample
         sraw += S.pm[w][1];
         corr += S.pm[w][2];
       }
-      const double sH = fmax(0.0, sh_row - sraw + spen);
+      sH = fmax(0.0, sh_row - sraw + spen);
       const double S_prod = a.total_expsum[row];
       const double Stot = S_prod + corr;
-      imprecise = a.summary_raw && S_prod > 16.0 * Stot;
       const bool tail_empty = a.V == a.H;
       bool degenerate = false;
       if (!tail_empty) {
         if (!(Stot > 0.0) || !isfinite(Stot)) degenerate = true;
         else alpha = fmin(sH / Stot, 1.0);
       }
-      const bool accept = !degenerate && sH > 0.0 && (tail_empty || u[1] <= alpha);
+      deferred = sH > 0.0 && defer_accept(a, S_prod, Stot, alpha, u[1]);
+      const bool accept = deferred || (!degenerate && sH > 0.0 && (tail_empty || u[1] <= alpha));
       if (!accept) {
         if (threadIdx.x == 0) {
           uint8_t fl = DP_FLAG_REJECTED;
           if (degenerate || (tail_empty && !(sH > 0.0))) fl |= DP_FLAG_DEGENERATE;
-          else if (fabs(u[1] - alpha) < kBoundaryEps || imprecise) fl |= DP_FLAG_NEAR_BOUNDARY;
+          else if (fabs(u[1] - alpha) < kBoundaryEps) fl |= DP_FLAG_NEAR_BOUNDARY;
           a.flags[row] = fl;
           if (a.dbg.alpha) a.dbg.alpha[row] = alpha;
           if (a.dbg.margin) a.dbg.margin[row] = fabs(u[1] - alpha);
@@ -576,8 +576,8 @@ __global__ void __launch_bounds__(kMW * 32, kMWBlocks) warp_sample_kernel(Sample
       a.logprob[row] = d.logprob;
       uint8_t fl = MODE == kHot ? DP_FLAG_ACCEPTED_HOT : 0;
       double margin = d.margin;
-      if (MODE == kHot && a.V != a.H) margin = fmin(margin, fabs(u[1] - alpha));
-      if (margin < kBoundaryEps || imprecise) fl |= DP_FLAG_NEAR_BOUNDARY;
+      if (MODE == kHot && a.V != a.H && !deferred) margin = fmin(margin, fabs(u[1] - alpha));
+      if (margin < kBoundaryEps) fl |= DP_FLAG_NEAR_BOUNDARY;
       a.flags[row] = fl;
       if (a.dbg.margin) a.dbg.margin[row] = margin;
       if (a.dbg.kept) a.dbg.kept[row] = d.kept;
@@ -585,7 +585,11 @@ __global__ void __launch_bounds__(kMW * 32, kMWBlocks) warp_sample_kernel(Sample
       if (a.dbg.bytes_touched) a.dbg.bytes_touched[row] = (uint64_t)n * sizeof(T);
       if (a.dbg.stats) atomicAdd((unsigned long long*)&a.dbg.stats[0], 1ull);
     }
-    warp_record_token(a, row, pos_to_id(a, (int64_t)fpos[d.index] + lo));   // fused K5
+    if (deferred) {
+      if (lane == 0) push_resum(a, row, sH);   // the exact re-sum decides, then records
+    } else {
+      warp_record_token(a, row, pos_to_id(a, (int64_t)fpos[d.index] + lo));   // fused K5
+    }
     if (a.dbg.topk_ids) {
       const int32_t m = min((int32_t)kk, a.dbg.topk_stride);
       for (int32_t j = lane; j < m; j += 32) {

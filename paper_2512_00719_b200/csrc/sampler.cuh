@@ -48,7 +48,19 @@ struct SampleArgs {
   int64_t shard_n;
   int32_t nshard;
   int32_t shard_per_cta;        // shards one CTA streams (nshard = split * shard_per_cta)
+  // kHot with a raw producer summary: rows whose accept test the cancelling
+  // correction cannot decide are listed here (hot decision written, penalty
+  // update withheld) and re-decided by the exact re-sum (resum_kernel)
+  int32_t* resum_rows;
+  int32_t* resum_count;
+  double* resum_sh;             // [B] the row's hot mass S_H (relative to row_max)
+  int32_t force_resum;          // DP_PLAN_FORCE_RESUM (test hook)
 };
+
+// upper bound of the penalty-list length over the call's rows (sizes lists)
+__host__ __device__ inline int32_t pen_bound(const dp_penalty_t& pen) {
+  return (pen.max_len > 0 && pen.max_len < pen.cap) ? pen.max_len : pen.cap;
+}
 
 DP_DEV int64_t dom_lo(const SampleArgs& a, int mode) { return mode == kTail ? a.H : 0; }
 DP_DEV int64_t dom_n(const SampleArgs& a, int mode) {
@@ -171,7 +183,7 @@ constexpr int kWarpPenCap = 256;  // penalty-list capacity it can hash
 
 DP_DEV bool warp_row_ok(const SampleArgs& a, int32_t k, int32_t plen, int64_t n) {
   return k > 0 && (int64_t)k < n && k <= kWarpKMax && min64(n, (int64_t)k + plen) <= kWarpKpMax &&
-         a.pen.cap <= kWarpPenCap;
+         plen <= kWarpPenCap;
 }
 DP_DEV int route_row(const SampleArgs& a, int mode, int32_t k, int32_t plen, int64_t n) {
   if (a.force_general) return kRouteGeneral;
@@ -202,6 +214,28 @@ DP_DEV double raw_summary_correction(const SampleArgs& a, int row, const dp_para
     c += exp(ready_penalized(x, pcnt[j], p) - mrow) - exp(ready_plain(x, p) - mrow);
   }
   return c;
+}
+
+// ---------------------------------------------------------------------------
+// SHVS accept test against a RAW producer summary (plan->summary_raw): the
+// ready total is S = S_prod + corr, where S_prod (the producer's sum of f32
+// exp terms, relative error <= kRawSumRelErr) may hold mostly mass that the
+// penalties have since removed.  The computed alpha = S_H / S then carries an
+// absolute error up to kRawSumRelErr * alpha * S_prod / S.  Whenever that
+// exceeds the 1e-6 decision band and the draw u_accept lies inside it — or S
+// came out non-positive — the accept test is deferred to an exact re-sum of
+// the penalized row (resum_kernel, summary.cu); every other row is decided
+// here (a decision inside the band is flagged NEAR_BOUNDARY as usual).
+constexpr double kRawSumRelErr = 1e-6;
+DP_DEV bool defer_accept(const SampleArgs& a, double S_prod, double S, double alpha, double u_accept) {
+  if (!a.summary_raw || a.resum_rows == nullptr || a.V == a.H) return false;
+  if (!(S > 0.0) || !isfinite(S) || a.force_resum) return true;
+  const double err = kRawSumRelErr * fmax(alpha, 1e-300) * (fabs(S_prod) / S);
+  return err > kBoundaryEps && fabs(u_accept - alpha) <= err;
+}
+DP_DEV void push_resum(const SampleArgs& a, int row, double sH) {
+  a.resum_sh[row] = sH;
+  a.resum_rows[atomicAdd(a.resum_count, 1)] = row;
 }
 
 // ---------------------------------------------------------------------------

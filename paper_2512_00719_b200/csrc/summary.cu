@@ -185,6 +185,89 @@ __global__ void __launch_bounds__(NT) hot_mass_curve_kernel(const T* logits, int
   }
 }
 
+// Exact re-decision of the SHVS accept tests that defer_accept (sampler.cuh)
+// left open: the row's ready total S relative to the producer's row max,
+// summed exactly (f64 exp of every ready value; penalized positions excluded
+// from the stream by a bitmap and added with their penalized values), then
+// alpha = S_H / S and the accept test of shvs.py:223-236.  An accepted row
+// keeps the hot decision the hot pass wrote and records its token (fused
+// update); a rejected one joins the reject list for the tail pass, which runs
+// after this kernel.
+template <typename T, int NT>
+__global__ void __launch_bounds__(NT) resum_kernel(SampleArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  double* redd = reinterpret_cast<double*>(smem);
+  uint32_t* bitmap = reinterpret_cast<uint32_t*>(smem + 40 * 8);
+  const int nrows = *a.resum_count;
+  const uint32_t words = (uint32_t)((a.V + 31) / 32);
+  for (int ridx = blockIdx.x; ridx < nrows; ridx += gridDim.x) {
+    const int row = a.resum_rows[ridx];
+    const dp_params_t p = a.params[row];
+    const int32_t plen = pen_len(a, row, p);
+    const int32_t* pids = a.pen.ids + (int64_t)row * a.pen.cap;
+    const int32_t* pcnt = a.pen.out_count + (int64_t)row * a.pen.cap;
+    const double mrow = a.row_max[row];
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < words; i += NT) bitmap[i] = 0u;
+    __syncthreads();
+    double s = 0.0;
+    for (int32_t j = threadIdx.x; j < plen; j += NT) {
+      const int64_t pos = id_to_pos(a, pids[j]);
+      atomicOr(&bitmap[pos >> 5], 1u << (pos & 31));
+      s += exp(ready_penalized(row_value<T>(a, row, pos), pcnt[j], p) - mrow);
+    }
+    __syncthreads();
+    for (int64_t pos = threadIdx.x; pos < a.V; pos += NT) {
+      if ((bitmap[pos >> 5] >> (pos & 31)) & 1u) continue;
+      s += exp(ready_plain(row_value<T>(a, row, pos), p) - mrow);
+    }
+    const double S = block_sum_f64<NT>(s, redd);
+    if (threadIdx.x == 0) {
+      double u[3];
+      get_uniforms(a, row, p, u);
+      const double sH = a.resum_sh[row];
+      const bool ok = S > 0.0 && isfinite(S);
+      const double alpha = ok ? fmin(sH / S, 1.0) : 1.0;
+      const bool near = fabs(u[1] - alpha) < kBoundaryEps;
+      if (a.dbg.alpha) a.dbg.alpha[row] = alpha;
+      if (a.dbg.bytes_touched) a.dbg.bytes_touched[row] += (uint64_t)a.V * sizeof(T);
+      if (a.dbg.stats) atomicAdd((unsigned long long*)&a.dbg.stats[2], 1ull);
+      if (!ok) {
+        a.token[row] = -1;
+        a.logprob[row] = 0.0;
+        a.flags[row] = DP_FLAG_REJECTED | DP_FLAG_DEGENERATE;
+      } else if (u[1] <= alpha) {
+        a.flags[row] |= near ? DP_FLAG_NEAR_BOUNDARY : 0;
+        if (a.dbg.margin) a.dbg.margin[row] = fmin(a.dbg.margin[row], fabs(u[1] - alpha));
+        thread_record_token(a, row, a.token[row]);   // fused K5
+      } else {
+        a.flags[row] = DP_FLAG_REJECTED | (near ? DP_FLAG_NEAR_BOUNDARY : 0);
+        if (a.dbg.margin) a.dbg.margin[row] = fabs(u[1] - alpha);
+        a.reject_rows[atomicAdd(a.reject_count, 1)] = row;
+      }
+    }
+  }
+}
+
+cudaError_t launch_resum(const SampleArgs& a, int dtype, cudaStream_t st) {
+  constexpr int NT = 256;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = a.n_rows < sms ? (a.n_rows > 0 ? a.n_rows : 1) : sms;
+  const size_t smem = 40 * 8 + (size_t)((a.V + 31) / 32) * 4;
+  if (dtype == DP_F32) {
+    auto k = resum_kernel<float, NT>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k<<<grid, NT, smem, st>>>(a);
+  } else {
+    auto k = resum_kernel<__nv_bfloat16, NT>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k<<<grid, NT, smem, st>>>(a);
+  }
+  return cudaGetLastError();
+}
+
 cudaError_t launch_row_summary(const void* logits, int dtype, int64_t B, int64_t V, int64_t ld,
                                const dp_params_t* params, const dp_penalty_t& pen, const int32_t* inv_perm,
                                double* row_max, double* total, cudaStream_t st) {

@@ -98,7 +98,48 @@ def run(vocab, batch, iters, params_of, variant, hot_ids=None, zipf=1.2, noise=0
                                      bf16=bf16, variant=variant, seed=seed)))
 
 
+# round-2 cases: the configurations the bench ships (SHVS tail clusters at the
+# real vocabulary, long penalty lists, wide top-k, a long heavy-penalty run)
+LONG_KINDS = [
+    dict(temperature=0.8, top_k=1024, top_p=0.95, rep_penalty=1.1, presence_penalty=0.5, frequency_penalty=0.1),
+    dict(temperature=0.9, top_k=5000, min_p=0.01, rep_penalty=1.2),
+    dict(temperature=0.8, top_k=50, top_p=0.9, min_p=0.05, rep_penalty=1.1, presence_penalty=0.5,
+         frequency_penalty=0.1),
+    dict(temperature=0.7, top_p=0.9, rep_penalty=1.3, frequency_penalty=0.2),
+]
+HEAVY = dict(temperature=0.7, top_k=40, top_p=0.95, rep_penalty=1.3, presence_penalty=1.5, frequency_penalty=1.0)
+
+
+def main_round2():
+    out = {}
+    # SHVS at V=152,064 / H=4,096 with odd-ranked hot ids: ~half the rows reject,
+    # more than the 74 resident tail clusters -> 4-CTA clusters loop over rows
+    src = SyntheticSource(EngineConfig(vocab_size=152064, seed=0))
+    hot = src.hot_ordering()[1::2][:4096].copy()
+    out["shvs_c2big"] = run(152064, 160, 2, lambda b: dict(C2_PARAMS, seed=b), "shvs", hot_ids=hot)
+    out["shvs_c2big"]["hot_ids"] = hot
+    # 2-4k unique prompt ids per row, top-k 1024 / 5000, full path and SHVS
+    out["long_full"] = run(32000, 16, 3, lambda b: dict(LONG_KINDS[b % 4], seed=b), "offload-truncate",
+                           prompt_len=3500)
+    src32 = SyntheticSource(EngineConfig(vocab_size=32000, seed=0))
+    hot32 = src32.hot_ordering()[:2048].copy()
+    out["long_shvs"] = run(32000, 16, 3, lambda b: dict(LONG_KINDS[b % 4], seed=b), "shvs", hot_ids=hot32,
+                           prompt_len=3500)
+    out["long_shvs"]["hot_ids"] = hot32
+    # 300 iterations of heavy presence / frequency penalties on spiky rows: the
+    # penalized mass leaves the producer's raw summary (summary_raw regime)
+    src8 = SyntheticSource(EngineConfig(vocab_size=8192, seed=0, zipf_exponent=1.6))
+    hot8 = src8.hot_ordering()[:1024].copy()
+    out["heavy_shvs"] = run(8192, 8, 300, lambda b: dict(HEAVY, seed=b), "shvs", hot_ids=hot8, zipf=1.6)
+    out["heavy_shvs"]["hot_ids"] = hot8
+    for name, d in out.items():
+        np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **d)
+        print(name, d["tokens"].shape, "accept", float(np.mean(d["accepted"])))
+
+
 def main():
+    if "--round2" in sys.argv:
+        return main_round2()
     out = {}
     # (1) C1 at full size: V=32000, B=64, tau .8, k 50, p .9, rep 1.1 (BASELINE configs[0])
     c1 = dict(temperature=0.8, top_k=50, top_p=0.9, rep_penalty=1.1)

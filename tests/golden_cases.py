@@ -31,6 +31,15 @@ C1 = dict(temperature=0.8, top_k=50, top_p=0.9, rep_penalty=1.1)
 C2 = dict(temperature=0.8, top_k=50, top_p=0.9, min_p=0.05, rep_penalty=1.1,
           presence_penalty=0.5, frequency_penalty=0.1)
 
+LONG_KINDS = [
+    dict(temperature=0.8, top_k=1024, top_p=0.95, rep_penalty=1.1, presence_penalty=0.5, frequency_penalty=0.1),
+    dict(temperature=0.9, top_k=5000, min_p=0.01, rep_penalty=1.2),
+    dict(temperature=0.8, top_k=50, top_p=0.9, min_p=0.05, rep_penalty=1.1, presence_penalty=0.5,
+         frequency_penalty=0.1),
+    dict(temperature=0.7, top_p=0.9, rep_penalty=1.3, frequency_penalty=0.2),
+]
+HEAVY = dict(temperature=0.7, top_k=40, top_p=0.95, rep_penalty=1.3, presence_penalty=1.5, frequency_penalty=1.0)
+
 CASES = {
     "c1_full": lambda b: C1,
     "het_full": lambda b: dict(KINDS[b % len(KINDS)], seed=b % 3),
@@ -39,6 +48,11 @@ CASES = {
     "shvs_reject": lambda b: dict(C2, seed=7),
     "shvs_neutral": lambda b: dict(seed=b),
     "c2_full": lambda b: C2,
+    # round 2: the shapes and regimes the bench ships (make_golden.py --round2)
+    "shvs_c2big": lambda b: dict(C2, seed=b),
+    "long_full": lambda b: dict(LONG_KINDS[b % 4], seed=b),
+    "long_shvs": lambda b: dict(LONG_KINDS[b % 4], seed=b),
+    "heavy_shvs": lambda b: dict(HEAVY, seed=b),
 }
 
 

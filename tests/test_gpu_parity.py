@@ -32,7 +32,7 @@ def torch_cuda():
     return torch
 
 
-def plane_for(torch, vocab, params, prompts, hot_ids=None, max_generated=64, split=0, kernel=0):
+def plane_for(torch, vocab, params, prompts, hot_ids=None, max_generated=65536, split=0, kernel=0):
     from paper_2512_00719_b200 import DecisionPlane, HotVocab, SamplingParams
 
     hot = HotVocab(vocab, hot_ids) if hot_ids is not None else None
@@ -59,15 +59,27 @@ def compare(tag, gpu_tok, gpu_lp, dec, exempt_log, lp_tol=1e-7):
     assert not bad, f"{tag}: token mismatches outside the boundary band: {bad[:8]}"
 
 
-def run_golden(torch, name, variant, raw_summary=False, kernel=0, storage="whole"):
+def run_golden(torch, name, variant, raw_summary=False, kernel=0, storage="whole", force_resum=False):
     case = Case(name)
     params = case.params()
     states = case.states()
     plane = plane_for(torch, case.vocab, params, [case.prompts[b] for b in range(case.batch)],
                       hot_ids=case.hot_ids, kernel=kernel)
     exempt = []
+    resummed = 0
     for it in range(case.iters):
         x = case.logits(it)
+        # alpha tolerance: a raw producer summary cancels when penalized ids
+        # held most of the raw mass; the reported alpha then carries an error
+        # up to 1e-6 * alpha * S_raw / S (the accept DECISION is still exact:
+        # undecidable rows are re-summed on the device)
+        a_tol = np.full(case.batch, 1e-6)
+        if raw_summary:
+            for b in range(case.batch):
+                r = O.ready_row(x[b], states[b], params[b])
+                raw = x[b].astype(np.float64) / params[b].temperature
+                mx = max(r.max(), raw.max())
+                a_tol[b] = max(1e-6, 2e-6 * np.exp(raw - mx).sum() / np.exp(r - mx).sum())
         dec = O.sample_batch(x, states, params, list(range(case.batch)), it, path=case.path,
                              hot_ids=case.hot_ids)
         # oracle == reference run (pinned on CPU); the GPU must match both
@@ -77,7 +89,8 @@ def run_golden(torch, name, variant, raw_summary=False, kernel=0, storage="whole
             xt = plane.hot.to_hot_first(xt).contiguous()
         summ = plane.producer_summary(xt) if raw_summary else None
         if storage == "whole":
-            d = plane.sample(xt, it, variant=variant, debug=True, summary=summ, summary_raw=raw_summary)
+            d = plane.sample(xt, it, variant=variant, debug=True, summary=summ, summary_raw=raw_summary,
+                             force_resum=force_resum)
         else:
             # split storage: hot prefix on the device, tail on the device or in
             # pinned host memory (read zero-copy by the tail pass)
@@ -91,13 +104,16 @@ def run_golden(torch, name, variant, raw_summary=False, kernel=0, storage="whole
             d = plane.sample_split(hot, tail, it, summ, debug=True, summary_raw=raw_summary)
         tok, lp = d.token.cpu().numpy(), d.logprob.cpu().numpy()
         compare(f"{name}/it{it}", tok, lp, dec, exempt)
+        if d.stats is not None:
+            resummed += int(d.stats[2])
+            d.stats.zero_()
         fl = d.flags.cpu().numpy()
         if variant == "shvs":
             acc = (fl & 0x02) != 0
             for b, dd in enumerate(dec):
                 if dd.margin >= EPS:
                     assert acc[b] == dd.accepted_hot, (name, it, b)
-                    assert abs(d.alpha.cpu().numpy()[b] - dd.alpha) < 1e-6
+                    assert abs(d.alpha.cpu().numpy()[b] - dd.alpha) < a_tol[b], (b, a_tol[b])
         # keep GPU penalty state identical to the oracle's even for exempt rows
         if not np.array_equal(tok, [dd.token for dd in dec]):
             for b, dd in enumerate(dec):
@@ -112,6 +128,7 @@ def run_golden(torch, name, variant, raw_summary=False, kernel=0, storage="whole
             assert dict(zip(ids.tolist(), cnt.tolist())) == want
     if exempt:
         print("boundary exemptions:", exempt)
+    return resummed
 
 
 def test_uniforms_bit_exact(torch_cuda, golden_dir):
@@ -635,3 +652,232 @@ def test_tp_sharded_multi_shard_ctas_match_stitched(torch_cuda, t, bf16):
                              O.uniforms_per_row([params[r].seed], 0, [r])[0]) for r in rows]
     exempt = []
     compare(f"tp{t}-multi", d.token.cpu().numpy()[rows], d.logprob.cpu().numpy()[rows], dec, exempt, lp_tol=1e-6)
+
+
+# ---------------------------------------------------------------------------
+# round 2: the configurations the bench ships
+
+
+@pytest.mark.parametrize("raw", [False, True])
+def test_shvs_tail_clusters_at_c2_vocab_match_reference_run(torch_cuda, raw):
+    """SHVS at V=152,064, H=4,096 (odd-ranked hot ids, ~63% of 160 rows
+    reject): the tail pass runs 4-CTA clusters that loop over more rejected
+    rows than there are resident clusters (mbarrier phase flips)."""
+    run_golden(torch_cuda, "shvs_c2big", "shvs", raw_summary=raw)
+
+
+@pytest.mark.parametrize("name,variant", [("long_full", "full"), ("long_shvs", "shvs")])
+def test_long_penalty_lists_and_wide_top_k_match_reference_run(torch_cuda, name, variant):
+    """2-4k unique prompt ids per row, top-k 1024 / 5000 / 50 / off."""
+    run_golden(torch_cuda, name, variant)
+
+
+@pytest.mark.parametrize("raw,force", [(False, False), (True, False), (True, True)])
+def test_heavy_penalties_300_iterations_match_reference_run(torch_cuda, raw, force):
+    """300 iterations of heavy presence / frequency penalties on spiky rows:
+    the producer's raw summary holds ~400-900x the penalized mass, so the
+    on-device correction cancels catastrophically; rows whose accept test
+    cannot be decided from it (|u - alpha| within the correction's error) are
+    re-summed exactly — no exemption.  This run has none naturally (closest
+    row: 1.16x the error bound, computed with the oracle), so `force` routes
+    EVERY accept test through the exact re-sum (DP_PLAN_FORCE_RESUM) and the
+    decisions must still equal the reference's."""
+    resummed = run_golden(torch_cuda, "heavy_shvs", "shvs", raw_summary=raw, force_resum=force)
+    print("accept tests re-summed exactly:", resummed)
+    if force:
+        assert resummed == 8 * 300   # every row, every iteration
+
+
+def _bench_params(cfg_mix, b):
+    C2 = dict(temperature=0.8, top_k=50, top_p=0.9, min_p=0.05, rep_penalty=1.1, presence_penalty=0.5,
+              frequency_penalty=0.1)
+    if not cfg_mix:
+        return O.Params(**C2, seed=0)
+    mix = [dict(temperature=0.8, top_k=1), dict(temperature=0.8, top_k=50), dict(temperature=0.8, top_p=0.9),
+           dict(temperature=0.8, min_p=0.05), C2]
+    kw = dict(mix[b % 5])
+    if (b // 5) % 2 == 1:
+        kw.update(rep_penalty=1.1, presence_penalty=0.5, frequency_penalty=0.1)
+    return O.Params(**kw, seed=0)
+
+
+def _big_batch_parity(torch, v, bsz, bf16, mix, variant, hot_size, check_every, iters=2, raw=True):
+    from paper_2512_00719_b200 import DecisionPlane, HotVocab, SamplingParams
+    from paper_2512_00719_b200.synthetic import SyntheticSource
+
+    params = [_bench_params(mix, b) for b in range(bsz)]
+    prompts = [np.random.default_rng(b).integers(0, v, 32) for b in range(bsz)]
+    src = SyntheticSource(v, device="cuda")
+    hot = HotVocab(v, src.hot_ordering()[:hot_size]) if variant == "shvs" else None
+    plane = DecisionPlane(v, [SamplingParams(**vars(p)) for p in params], prompts=prompts, hot=hot)
+    check = list(range(0, bsz, check_every))
+    states = {b: O.State.new(prompts[b], v) for b in check}
+    tail = O.tail_ids_of(hot.hot_ids, v) if hot is not None else None
+    perm, inv = hot.device_maps(plane.device) if hot is not None else (None, None)
+    exempt, rejected = [], 0
+    dt = torch.bfloat16 if bf16 else torch.float32
+    for it in range(iters):
+        x = src.generate(it, range(bsz), dtype=dt, perm=perm)
+        if variant == "shvs":
+            summ = plane.producer_summary(x) if raw else None
+            d = plane.sample(x, it, variant="shvs", summary=summ, summary_raw=raw and summ is not None)
+        else:
+            d = plane.sample(x, it)
+        tok, lp, fl = d.token.cpu().numpy(), d.logprob.cpu().numpy(), d.flags.cpu().numpy()
+        assert not (fl & 0x80).any()
+        rejected += int(((fl & 0x08) != 0).sum())
+        xh = x[check].float().cpu().numpy()
+        if inv is not None:
+            xh = xh[:, inv.cpu().numpy()]          # back to token-id order
+        dec = []
+        for i, b in enumerate(check):
+            u = O.uniforms_per_row([params[b].seed], it, [b])[0]
+            if variant == "shvs":
+                dec.append(O.sample_shvs_row(xh[i], states[b], params[b], u, hot.hot_ids, tail))
+            else:
+                dec.append(O.sample_full_row(xh[i], states[b], params[b], u))
+        compare(f"big/{variant}/V{v}/B{bsz}/it{it}", tok[check], lp[check], dec, exempt, lp_tol=1e-6)
+        for b in check:
+            states[b].update(int(tok[b]))
+        del x
+    print("exemptions:", exempt, "rejected rows:", rejected)
+    return rejected
+
+
+@pytest.mark.parametrize("variant", ["shvs", "full"])
+def test_c5_full_batch_bf16_mix_matches_oracle(torch_cuda, variant):
+    """C5 at full size: V=152,064, B=16,384 bf16, the 5-way row mix with
+    penalties alternating, SHVS at H=4,096 with the producer's raw summary
+    (and the full path); 512 rows checked against the oracle per iteration."""
+    _big_batch_parity(torch_cuda, 152064, 16384, True, True, variant, 4096, 32)
+    import torch
+    torch.cuda.empty_cache()
+
+
+def test_c4_full_batch_matches_oracle(torch_cuda):
+    """C4 at full size on one GPU: V=151,936, B=8,192 fp32, C2 knobs; 256 rows."""
+    _big_batch_parity(torch_cuda, 151936, 8192, False, False, "full", 0, 32)
+    import torch
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("raw", [False, True])
+def test_c2_shvs_bench_config_matches_oracle(torch_cuda, raw):
+    """The bench's SHVS line: C2 at full size, H=4,096 hot head."""
+    _big_batch_parity(torch_cuda, 152064, 1024, False, False, "shvs", 4096, 8, raw=raw)
+
+
+# ---------------------------------------------------------------------------
+# drop-in surface: the reference's worker loop with our objects substituted
+
+
+@pytest.mark.parametrize("name", ["c1_full", "het_full", "het_shvs", "shvs_reject", "long_full"])
+def test_reference_worker_loop_with_dropin_sampler(torch_cuda, name):
+    """The reference's per-row worker loop (service.py:752-766 /
+    harness.py:266-279: make_shard_blocks -> assemble_view -> per row
+    pregenerate_slice -> _Sampler.sample -> update_output_histogram) with this
+    package's objects in place of the reference's.  Tokens equal the fixture
+    the reference itself produced."""
+    from paper_2512_00719_b200 import (HotVocab, SamplingParams, _Sampler, assemble_view, make_shard_blocks,
+                                       new_sequence_state, update_output_histogram)
+    from paper_2512_00719_b200 import rng
+
+    torch = torch_cuda
+    case = Case(name)
+    v, bsz = case.vocab, case.batch
+    states = [new_sequence_state(b, case.prompts[b].tolist(), v) for b in range(bsz)]
+    hot = HotVocab(v, case.hot_ids if case.hot_ids is not None else np.arange(v))
+    sampler = _Sampler("shvs" if case.path == "shvs" else "offload-truncate", hot)
+    ostates, oparams = case.states(), case.params()
+    exempt = []
+    for it in range(case.iters):
+        x = case.logits(it)
+        blocks = make_shard_blocks(1, it, torch.from_numpy(x).cuda(), states,
+                                   lambda b: SamplingParams(**case.params_of(b)))
+        view = assemble_view(blocks, (0, bsz))
+        toks, lps = [], []
+        for b in range(bsz):
+            p = SamplingParams(**case.params_of(b))
+            draws = rng.pregenerate_slice(p.seed, it, [b])[0].cpu().numpy()
+            d = sampler.sample(view, b, b, states[b], p, draws, it)
+            update_output_histogram(states[b], d.token_id)
+            toks.append(d.token_id)
+            lps.append(d.logprob)
+        dec = O.sample_batch(x, ostates, oparams, list(range(bsz)), it, path=case.path, hot_ids=case.hot_ids)
+        compare(f"dropin/{name}/it{it}", toks, lps, dec, exempt, lp_tol=1e-6)
+        if exempt:
+            pytest.skip(f"boundary-exempt rows diverge state: {exempt}")
+        np.testing.assert_array_equal(toks, case.tokens[it])
+
+
+def test_reference_objects_drive_dropin_sampler(torch_cuda):
+    """The reference's OWN objects (SequenceState, SamplingParams, HotVocab,
+    make_shard_blocks, assemble_view, update_output_histogram from the
+    unmodified install in baseline/_ref) with only _Sampler swapped."""
+    import os
+    import sys
+
+    ref = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "decplane")):
+        pytest.skip("reference not installed in baseline/_ref")
+    sys.path.insert(0, ref)
+    from decplane import rng as R
+    from decplane.core import SamplingParams as RP
+    from decplane.core import new_sequence_state as r_new
+    from decplane.penalty import update_output_histogram as r_update
+    from decplane.service import EngineConfig, make_shard_blocks as r_blocks
+    from decplane.shvs import HotVocab as RHot
+    from decplane.transport import assemble_view as r_view
+
+    from paper_2512_00719_b200 import _Sampler
+
+    for name in ("het_shvs", "c1_full"):
+        case = Case(name)
+        v, bsz = case.vocab, case.batch
+        states = [r_new(b, case.prompts[b].tolist(), v) for b in range(bsz)]
+        hot = RHot(v, case.hot_ids if case.hot_ids is not None else np.arange(v))
+        sampler = _Sampler("shvs" if case.path == "shvs" else "offload-truncate", hot)
+        cfg = EngineConfig(vocab_size=v, batch_size=bsz)
+        for it in range(case.iters):
+            x = case.logits(it)
+            blocks = r_blocks(cfg, it, x.T.astype(np.float64), states, lambda b: RP(**case.params_of(b)))
+            view = r_view(blocks, (0, bsz))
+            toks = []
+            for b in range(bsz):
+                p = RP(**case.params_of(b))
+                d = sampler.sample(view, b, b, states[b], p, R.pregenerate_slice(p.seed, it, [b])[0], it)
+                r_update(states[b], d.token_id)
+                toks.append(d.token_id)
+            np.testing.assert_array_equal(toks, case.tokens[it], err_msg=f"{name}/it{it}")
+
+
+def test_dropin_sample_full_and_shvs_sample(torch_cuda):
+    """filtering.sample_full and shvs.shvs_sample signatures on single rows."""
+    from paper_2512_00719_b200 import HotVocab, SamplingParams, ShvsRowContext, new_sequence_state, \
+        sample_full, shvs_sample, update_output_histogram
+
+    case = Case("c1_full")
+    v = case.vocab
+    x = case.logits(0)
+    for b in range(6):
+        st = new_sequence_state(b, case.prompts[b].tolist(), v)
+        p = SamplingParams(**case.params_of(b))
+        u = O.uniforms_per_row([p.seed], 0, [b])[0]
+        d = sample_full(x[b], st, p, u, iteration_id=0)
+        want = O.sample_full_row(x[b], O.State.new(case.prompts[b], v), O.Params(**case.params_of(b)), u)
+        assert d.token_id == want.token or want.margin < EPS
+        update_output_histogram(st, d.token_id)
+        assert st.generated_len == 1
+    # shvs_sample on a sampling-ready row (tau folded, no penalties): f32-exact values
+    src = O.Synthetic(8192)
+    hot_ids = src.rank_to_token[:1024]
+    hot = HotVocab(8192, hot_ids)
+    tail = O.tail_ids_of(hot_ids, 8192)
+    row = src.wire(3, [0])[0]
+    for k in (0, 50):
+        p = O.Params(top_k=k, top_p=0.9, seed=5)
+        u = O.uniforms_per_row([5], 3, [0])[0]
+        m, s_tot = O.row_summary(row.astype(np.float64))
+        d = shvs_sample(ShvsRowContext(row, m, s_tot), hot, SamplingParams(**vars(p)), u, 3, 0)
+        want = O.sample_shvs_row(row, O.State.new([], 8192), p, u, hot_ids, tail)
+        assert (d.token_id == want.token and d.accepted_hot == want.accepted_hot) or want.margin < EPS

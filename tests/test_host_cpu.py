@@ -43,8 +43,8 @@ def test_struct_layouts_match_header():
 
     assert C.sizeof(N.Params) == 64
     assert N.Params.top_p.offset == 16 and N.Params.seed.offset == 56
-    assert C.sizeof(N.Penalty) == 40
-    assert C.sizeof(N.Plan) == 32
+    assert C.sizeof(N.Penalty) == 48 and N.Penalty.max_len.offset == 40
+    assert C.sizeof(N.Plan) == 48 and N.Plan.workspace.offset == 32 and N.Plan.workspace_len.offset == 40
 
 
 def test_library_rejects_bad_arguments_without_gpu(lib):
@@ -56,7 +56,7 @@ def test_library_rejects_bad_arguments_without_gpu(lib):
     st = lib.dp_sample_full(None, 0, 1, 10, 10, None, None, None, None, 0, None, None, None, None, None, None)
     assert st == N.DP_ERR_ARG
     assert b"null" in lib.dp_last_error()
-    pen = N.Penalty(1, 1, 1, 1, 4, 99)
+    pen = N.Penalty(1, 1, 1, 1, 4, 99, 0, 0)
     st = lib.dp_sample_full(C.c_void_p(1), 0, 1, 10, 10, C.c_void_p(1), C.byref(pen), None, C.c_void_p(1), 0,
                             C.c_void_p(1), C.c_void_p(1), C.c_void_p(1), None, None, None)
     assert st == N.DP_ERR_ARG and b"penalty" in lib.dp_last_error()
@@ -73,7 +73,7 @@ def test_sharded_entry_checks_tiling_without_gpu(lib):
     from paper_2512_00719_b200 import _native as N
 
     one = C.c_void_p(1)
-    pen = N.Penalty(1, 1, 1, 1, 4, 12)
+    pen = N.Penalty(1, 1, 1, 1, 4, 12, 0, 0)
 
     def call(ptrs, t, v, ld):
         arr = (C.c_void_p * max(len(ptrs), 1))(*ptrs)
