@@ -7,8 +7,10 @@ A step = one pass of the hot path over the batch: dp_sample_full (fused
 penalties -> tau -> top-k -> top-p -> min-p -> draw, with the penalty-state
 update fused into the deciding kernel) — the reference's timed unit,
 sample + update_output_histogram (harness.py:274-279).  With N GPUs each rank
-owns a fixed 1,024-row slice (weak scaling) and the step ends with the
-token-id all-gather over NCCL.
+runs BASELINE configs[3] (C4: V=151,936, B=8,192 split over the ranks by
+partition_batch, strong scaling) and the step ends with the token-id
+all-gather over NCCL, inside the timed region.  `--gpus N` without a launcher
+re-execs itself under torch.distributed.run (one process per GPU).
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
                     [--config c2|c1|c3|c4|c5] [--variant full|shvs]
@@ -52,6 +54,27 @@ RESET_EVERY = 128  # harness.py:266-269
 
 def env_rank():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def _free_port() -> int:
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def self_launch(n: int) -> int:
+    """`bench.py --gpus N` without a launcher: re-exec this command under
+    torch.distributed.run with N local ranks (one process per GPU, rendezvous
+    on 127.0.0.1).  NCCL's INIT lines (rank / nranks of every communicator)
+    go to stderr so the rank count can be checked."""
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
 
 
 def measured_peak():
@@ -277,7 +300,8 @@ def reference_arm(args, cfg):
             if kind == "reference" else "oracle port of _Sampler.sample + update_output_histogram")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * cfg["B"] / value,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong" if cfg.get("strong") else "weak",
+            "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (SyntheticSource formula, seed 0)",
             "config": {"workload": cfg["name"], "V": v, "B": cfg["B"], "params": cfg["params"]},
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": kind,
@@ -660,7 +684,8 @@ def main():
     ap.add_argument("--hot", type=int, default=4096,
                     help="SHVS hot-set size (4,096: the measured optimum of tools/c3_sweep.py on this source)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=None, choices=sorted(CONFIGS),
+                    help="default: c2 on one GPU, c4 (B=8,192 split over the ranks, strong scaling) on N > 1")
     ap.add_argument("--variant", default="full", choices=["full", "shvs"])
     ap.add_argument("--split", type=int, default=0)
     ap.add_argument("--kernel", type=int, default=0, help="dp_plan_t.kernel: 0 auto, 1 CTA/cluster, 2 warp-per-row")
@@ -671,6 +696,11 @@ def main():
     ap.add_argument("--no-shvs", action="store_true", help="skip the SHVS sub-measurement of the full-path line")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args.gpus))
+    _, world, _ = env_rank()
+    if args.config is None:
+        args.config = "c2" if world == 1 else "c4"
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         reference_arm(args, cfg)
