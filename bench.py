@@ -465,7 +465,7 @@ def run_ours(args, cfg):
     if world > 1:
         dist.barrier()
     from paper_2512_00719_b200 import DecisionPlane, HotVocab
-    from paper_2512_00719_b200.sharded import BatchShard
+    from paper_2512_00719_b200.sharded import BatchShard, NcclTokenGather
     from paper_2512_00719_b200.synthetic import SyntheticSource
 
     v = cfg["V"]
@@ -489,6 +489,8 @@ def run_ours(args, cfg):
     gathered = torch.empty(shard.batch_size, dtype=torch.int32, device=dev)
     tok_pp = [torch.empty(b_local, dtype=torch.int32, device=dev) for _ in range(2)]
     gstream = torch.cuda.Stream(device=dev)
+    # the token all-gather through the library's C ABI (dp_allgather_tokens)
+    gather = NcclTokenGather(shard, dev) if world > 1 else None
     base_it = [0]
     # SHVS: the producer emits a penalty-free row summary with the logits
     # (LM-head epilogue); the sampler corrects it for the penalty list, so a
@@ -519,7 +521,7 @@ def run_ours(args, cfg):
             tok_pp[it & 1].copy_(d.token)
             gstream.wait_stream(cur)
             with torch.cuda.stream(gstream):
-                shard.gather(tok_pp[it & 1], out=gathered)
+                gather(tok_pp[it & 1], out=gathered)
         return d
 
     def join():
@@ -608,7 +610,7 @@ def run_ours(args, cfg):
         else:
             dd = plane.sample(dbuf, 10_000 + k)
         if world > 1:
-            shard.gather(dd.token, out=gathered)
+            gather(dd.token, out=gathered)
             tok_host.copy_(gathered[shard.lo:shard.hi], non_blocking=True)
         else:
             tok_host.copy_(dd.token, non_blocking=True)
@@ -672,6 +674,7 @@ def run_ours(args, cfg):
         }
         print(json.dumps(line), flush=True)
     if world > 1:
+        gather.close()
         dist.destroy_process_group()
 
 

@@ -18,7 +18,7 @@ PKG = os.path.join(ROOT, "paper_2512_00719_b200")
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIBDIR, "libdecplane_b200.so")
-SOURCES = ["capi.cu", "sample_topk.cu", "sample_warp.cu", "sample_general.cu", "summary.cu", "aux_kernels.cu"]
+SOURCES = ["capi.cu", "sample_topk.cu", "sample_warp.cu", "sample_general.cu", "summary.cu", "aux_kernels.cu", "collective.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -62,7 +62,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str | Non
         if verbose:
             sys.stderr.write(r.stderr)
     os.makedirs(os.path.dirname(lib), exist_ok=True)
-    link = [NVCC, *ARCH, "--shared", "-o", lib + ".tmp"] + [obj for _, obj, _ in results]
+    link = [NVCC, *ARCH, "--shared", "-o", lib + ".tmp"] + [obj for _, obj, _ in results] + ["-ldl"]
     r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

@@ -273,10 +273,21 @@ DP_API int dp_hot_mass_curve(const void* logits_hotfirst, int dtype, int64_t B, 
 DP_API int dp_encode_decisions(const int32_t* token, const double* logprob, const uint8_t* flags,
                                const uint64_t* seq_ids, int64_t B, uint8_t* out, void* stream);
 
-/* Token-id all-gather across batch shards (DecisionLedger, transport.py:400-433):
- * ncclAllGather of int32 tokens over the communicator `nccl_comm` (an
- * ncclComm_t).  Implemented in the host layer via torch.distributed; kept in
- * the ABI for non-Python callers that link NCCL themselves. */
+/* Token-id all-gather across batch shards (partition_batch + DecisionLedger,
+ * transport.py:133-144, :400-433; service.py:743-748): one ncclAllGather of
+ * rows_per_rank int32 tokens per rank into global[world * rows_per_rank], in
+ * rank order, on `stream`.  `comm` is an ncclComm_t (dp_nccl_comm_init, or the
+ * caller's own).  NCCL is resolved at run time (dlopen libnccl.so.2, reusing a
+ * copy already loaded in the process); without it these return
+ * DP_ERR_UNSUPPORTED.  dp_nccl_unique_id writes the 128-byte ncclUniqueId that
+ * rank 0 hands to every rank out of band; dp_nccl_comm_init runs on the
+ * caller's current device. */
+DP_API int dp_nccl_available(void);
+DP_API int dp_nccl_unique_id(uint8_t* id128);
+DP_API int dp_nccl_comm_init(void** comm, int32_t nranks, const uint8_t* id128, int32_t rank);
+DP_API int dp_nccl_comm_destroy(void* comm);
+DP_API int dp_allgather_tokens(const int32_t* local, int32_t* global, int64_t rows_per_rank, void* comm,
+                               void* stream);
 
 #ifdef __cplusplus
 }

@@ -188,6 +188,14 @@ void plan_topk(dp::SampleArgs& a, const dp_plan_t* plan, int64_t B, int64_t n, i
 
 }  // namespace
 
+namespace dp {
+// other translation units (collective.cu) report through dp_last_error
+int set_last_error(int code, const char* msg) {
+  std::snprintf(g_err, sizeof(g_err), "%s", msg);
+  return code;
+}
+}  // namespace dp
+
 extern "C" {
 
 int dp_version(void) { return 100; }

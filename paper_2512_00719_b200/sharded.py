@@ -90,4 +90,69 @@ class BatchShard:
         return full
 
 
-__all__ = ["BatchShard"]
+class NcclTokenGather:
+    """The token all-gather through the library's C ABI (dp_allgather_tokens,
+    SURVEY §8(b)): one ncclAllGather of int32 ids per iteration on a
+    communicator the library creates over NCCL (resolved at run time, the
+    copy torch already loaded).  Rank 0 draws the ncclUniqueId
+    (dp_nccl_unique_id) and hands it to the other ranks through the
+    torch.distributed group; every rank then joins on its own device.
+    Stream-ordered and CUDA-graph capturable like any NCCL collective."""
+
+    def __init__(self, shard: BatchShard, device, group=None):
+        import ctypes as C
+
+        import torch
+
+        from . import _native as N
+
+        self.shard, self.device = shard, torch.device(device)
+        lib = N.load()
+        if not lib.dp_nccl_available():
+            raise N.NativeUnavailable("dp_allgather_tokens needs libnccl.so.2")
+        uid = (C.c_uint8 * 128)()
+        if shard.rank == 0:
+            N.check(lib.dp_nccl_unique_id(uid), "dp_nccl_unique_id")
+        if shard.world > 1:
+            import torch.distributed as dist
+
+            box = [bytes(uid)]
+            dist.broadcast_object_list(box, src=0, group=group)
+            C.memmove(uid, box[0], 128)
+        self._comm = C.c_void_p()
+        with torch.cuda.device(self.device):
+            N.check(lib.dp_nccl_comm_init(C.byref(self._comm), shard.world, uid, shard.rank), "dp_nccl_comm_init")
+            self._pad = torch.zeros(shard.block, dtype=torch.int32, device=self.device)
+            self._full = torch.empty(shard.block * shard.world, dtype=torch.int32, device=self.device)
+        self._lib, self._N = lib, N
+
+    def __call__(self, local, out=None):
+        """[rows] int32 CUDA tensor of this rank -> [B] in batch order (on the
+        current stream of the plane's device)."""
+        import ctypes as C
+
+        import torch
+
+        sh = self.shard
+        if local.shape[0] != sh.rows or local.dtype != torch.int32 or local.device != self.device:
+            raise ValueError(f"rank {sh.rank} gathers its {sh.rows} int32 tokens on {self.device}")
+        src = local.contiguous()
+        if sh.rows < sh.block:
+            self._pad[: sh.rows].copy_(src)
+            src = self._pad
+        st = torch.cuda.current_stream(self.device).cuda_stream
+        self._N.check(self._lib.dp_allgather_tokens(C.c_void_p(src.data_ptr()), C.c_void_p(self._full.data_ptr()),
+                                                    sh.block, self._comm, C.c_void_p(st)), "dp_allgather_tokens")
+        full = self._full if sh.uniform else self._full.index_select(0, sh._keep_index(self.device))
+        if out is not None:
+            out.copy_(full)
+            return out
+        return full
+
+    def close(self) -> None:
+        if self._comm:
+            self._N.check(self._lib.dp_nccl_comm_destroy(self._comm), "dp_nccl_comm_destroy")
+            self._comm = None
+
+
+__all__ = ["BatchShard", "NcclTokenGather"]

@@ -165,3 +165,18 @@ def test_synthetic_hot_ordering_matches_oracle():
     for v in (16, 2048, 32000):
         np.testing.assert_array_equal(hot_ordering(0, v), O.synthetic_hot_ordering(0, v))
         np.testing.assert_array_equal(hot_ordering(5, v), O.synthetic_hot_ordering(5, v))
+
+
+def test_collective_entry_points_resolve_nccl(lib):
+    """dp_allgather_tokens' NCCL is found at run time (no GPU needed to draw a
+    unique id); bad arguments fail with DP_ERR_ARG before touching NCCL."""
+    import ctypes as C
+
+    from paper_2512_00719_b200 import _native as N
+
+    assert lib.dp_nccl_available() == 1
+    uid = (C.c_uint8 * 128)()
+    assert lib.dp_nccl_unique_id(uid) == N.DP_OK
+    assert any(bytes(uid))
+    assert lib.dp_allgather_tokens(None, None, 4, None, None) == N.DP_ERR_ARG
+    assert lib.dp_allgather_tokens(None, None, 0, C.c_void_p(1), None) == N.DP_OK
