@@ -354,27 +354,87 @@ def _timed(g, dist=None, world=1):
     return ms
 
 
+SIZING_GRID = (256, 512, 1024, 2048, 4096, 8192, 16384, 32768)
+
+
+def shvs_hot_size(args, plane, src, seq_ids, dev, dtype):
+    """The hot size SHVS runs at: `--hot H`, or (default) the paper's sizing
+    model on this workload — control.HotSizeController calibrates the hot
+    path's cost on the GPU at every grid size, measures the hit-ratio curve
+    of the current rows with K6 and takes sizing.optimal_hot_size (untimed
+    setup, like the reference's fit-sizing step, cli.py:70-95).  Leaves the
+    plane's hot set at that size."""
+    import torch
+
+    from paper_2512_00719_b200 import HotVocab
+    from paper_2512_00719_b200.control import HotSizeController
+
+    v = plane.vocab_size
+    master = HotVocab(v, src.hot_ordering())
+    if args.hot > 0:
+        plane.set_hot(master.resize(args.hot))
+        return args.hot, {"chosen_by": "--hot"}
+    plane.set_hot(master.resize(4096))
+    ctl = HotSizeController(plane, master, grid=SIZING_GRID)
+    xm = src.generate(0, seq_ids, perm=master.device_maps(dev)[0], dtype=dtype)
+    c0, c = ctl.calibrate_cost(xm)
+    h = ctl.refit(xm)
+    ctl.begin_iteration(0)
+    del xm
+    torch.cuda.empty_cache()
+    curve = ctl.model.curve
+    return h, {"chosen_by": "sizing model (control.HotSizeController: GPU-timed hot-path cost fit + K6 "
+                            "hit-ratio curve, sizing.optimal_hot_size)",
+               "grid": [int(g) for g in curve.grid], "alpha_bar": [round(float(a), 6) for a in curve.alpha_bar],
+               "c0_s_per_row": c0, "c_s_per_row_token": c, "hot_size": h,
+               "cost_points_s_per_row": [[int(hh), t] for hh, t in ctl.cost_points]}
+
+
+def _graph_ms(fn, k):
+    """Device ms per call of fn(i), k calls captured in one graph and replayed."""
+    import torch
+
+    for i in range(2):
+        fn(i)
+    g = _graph(fn, k)
+    torch.cuda.synchronize()
+    return _timed(g) / k
+
+
 def measure_shvs_e2e(args, cfg, plane_kw, src, seq_ids, dev, shard, world):
     """SHVS (speculative hot-vocab sampling) on the same workload, the
-    paper's decision path: device step time (sample + penalty update, CUDA
-    graph) and end to end with HOST-resident hot-first logits — the hot prefix
-    is staged with one strided DMA, rejected rows' tails are read zero-copy
-    (dp_stage_hot + dp_sample_shvs_split).  The producer's penalty-free row
-    summary travels with the logits (make_shard_blocks contract,
-    service.py:470-504)."""
+    paper's decision path, at the sizing model's hot size: device step time
+    (sample + penalty update, CUDA graph) and end to end with HOST-resident
+    hot-first logits — the hot prefix is staged with one strided DMA,
+    rejected rows' tails are read zero-copy (dp_stage_hot +
+    dp_sample_shvs_split).  The producer emits the penalty-free row summary
+    while it writes the logits (make_shard_blocks contract, service.py:470-504;
+    dp_synth_logits' fused summary): its marginal cost over the plain producer
+    is measured and added to the step ("with_summary"), and the cost of a
+    separate summary pass (dp_row_summary_raw) is reported beside it."""
     import torch
     import torch.distributed as dist
 
-    from paper_2512_00719_b200 import DecisionPlane, HotVocab
+    from paper_2512_00719_b200 import DecisionPlane
 
-    v, h = cfg["V"], args.hot
-    hot = HotVocab(v, src.hot_ordering()[:h])
-    plane = DecisionPlane(v, hot=hot, **plane_kw)
+    v = cfg["V"]
+    plane = DecisionPlane(v, **plane_kw)
     tdt = torch.float32 if cfg["dtype"] == "f32" else torch.bfloat16
+    h, sizing_info = shvs_hot_size(args, plane, src, seq_ids, dev, tdt)
     esz = 4 if cfg["dtype"] == "f32" else 2
-    perm = hot.device_maps(dev)[0]
-    bufs = [src.generate(i, seq_ids, dtype=tdt, perm=perm) for i in range(2)]
-    summ = [plane.producer_summary(b) for b in bufs]
+    perm = plane.hot.device_maps(dev)[0]
+    bufs, summ = [], []
+    for i in range(2):
+        x, sm = src.generate(i, seq_ids, dtype=tdt, perm=perm, summary_params=plane.params_dev)
+        bufs.append(x)
+        summ.append(sm)
+    # producer cost: plain generator vs generator + fused summary, and a separate summary pass
+    sd = torch.from_numpy(np.asarray(seq_ids, np.uint64).view(np.int64)).to(dev)
+    t_plain = _graph_ms(lambda i: src.generate(i, sd, dtype=tdt, perm=perm, out=bufs[i & 1]), 10)
+    t_fused = _graph_ms(lambda i: src.generate(i, sd, dtype=tdt, perm=perm, out=bufs[i & 1],
+                                               summary_params=plane.params_dev, summary_out=summ[i & 1]), 10)
+    t_sep = _graph_ms(lambda i: plane.producer_summary(bufs[i & 1]), 20)
+    fused_extra = max(0.0, t_fused - t_plain)
     base_it = [args.warmup]
 
     def step(i):
@@ -388,10 +448,11 @@ def measure_shvs_e2e(args, cfg, plane_kw, src, seq_ids, dev, shard, world):
     torch.cuda.synchronize()
     g = _graph(step, args.steps)
     ms = _timed(g, dist if world > 1 else None, world)
-    d = plane.sample(bufs[0], 0, variant="shvs", summary=summ[0], summary_raw=True, update=False)
+    d = plane.sample(bufs[0], 0, variant="shvs", summary=summ[0], summary_raw=True, update=False, debug=True)
     torch.cuda.synchronize()
     flags = d.flags.cpu().numpy()
     accept = float(np.mean((flags & 0x02) != 0))
+    bytes_row = float(d.bytes_touched.double().mean().item())
     rows = shard.rows
     # e2e: pinned host logits -> stage hot prefix -> sample (tail zero-copy) -> D2H tokens
     host = bufs[0].cpu().pin_memory()
@@ -405,7 +466,6 @@ def measure_shvs_e2e(args, cfg, plane_kw, src, seq_ids, dev, shard, world):
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st)
-    rej = 0
     for k in range(n_e2e):
         dd = plane.sample_host(host, 10_000 + k, sh, staging=staging, summary_raw=True)
         tok_host.copy_(dd.token, non_blocking=True)
@@ -418,8 +478,18 @@ def measure_shvs_e2e(args, cfg, plane_kw, src, seq_ids, dev, shard, world):
         e2e_ms, ms = float(t[0]), float(t[1])
     rej = int(((dd.flags.cpu().numpy() & 0x08) != 0).sum())
     tail_bytes = rej * (v - h) * esz
-    return {"hot_size": h, "accept": accept, "value": shard.batch_size * args.steps / (ms / 1000.0),
-            "ms_per_step": ms / args.steps,
+    step_ms = ms / args.steps
+    return {"hot_size": h, "sizing": sizing_info, "accept": accept,
+            "value": shard.batch_size * args.steps / (ms / 1000.0), "ms_per_step": step_ms,
+            "with_summary": {"ms_per_step": step_ms + fused_extra,
+                             "value": shard.batch_size / ((step_ms + fused_extra) / 1000.0),
+                             "summary": "producer-fused (dp_synth_logits emits (row_max, total_expsum) while "
+                                        "writing the logits); its marginal producer cost is added"},
+            "producer_ms": {"logits_only": t_plain, "logits_plus_fused_summary": t_fused,
+                            "fused_summary_marginal": fused_extra, "separate_summary_pass": t_sep},
+            "bytes_touched_per_row": {"measured_mean": bytes_row,
+                                      "algorithmic": h * esz + (1 - accept) * (v - h) * esz,
+                                      "source": "dp_debug_t.bytes_touched (kernel-counted loads per row)"},
             "e2e": {"value": shard.batch_size * n_e2e / (e2e_ms / 1000.0), "unit": "tokens/s",
                     "h2d_bytes_per_step": int(rows * h * esz + 16 * rows + tail_bytes),
                     "d2h_bytes_per_step": int(rows * 4), "steps": n_e2e,
@@ -479,24 +549,31 @@ def run_ours(args, cfg):
     params = [row_params(cfg, int(s)) for s in seq_ids]
     src = SyntheticSource(v, device=dev)
     variant = args.variant if not cfg.get("mix") else "shvs"
-    hot = HotVocab(v, src.hot_ordering()[: args.hot]) if variant == "shvs" else None
+    hot = None
     plane = DecisionPlane(v, params, prompts=prompts, seq_ids=seq_ids, hot=hot, device=dev,
                           max_generated=RESET_EVERY + 8, split=args.split, kernel=args.kernel)
     tdt = torch.float32 if cfg["dtype"] == "f32" else torch.bfloat16
+    sizing_info = None
+    if variant == "shvs":
+        hot_size, sizing_info = shvs_hot_size(args, plane, src, seq_ids, dev, tdt)
+        hot = plane.hot
     perm = hot.device_maps(dev)[0] if hot is not None else None
-    bufs = [src.generate(i, seq_ids, dtype=tdt, perm=perm) for i in range(2)]   # 2 x batch > L2
-    inv = hot.device_maps(dev)[1] if hot is not None else None
+    # 2 x batch > L2.  SHVS: the producer emits the penalty-free row summary
+    # while it writes the logits (dp_synth_logits' fused summary; the
+    # sampler corrects it for the penalty list), so a step streams only the
+    # hot prefix (+ tails of rejected rows)
+    summaries = None
+    if variant == "shvs":
+        gen = [src.generate(i, seq_ids, dtype=tdt, perm=perm, summary_params=plane.params_dev) for i in range(2)]
+        bufs, summaries = [g[0] for g in gen], [g[1] for g in gen]
+    else:
+        bufs = [src.generate(i, seq_ids, dtype=tdt, perm=perm) for i in range(2)]
     gathered = torch.empty(shard.batch_size, dtype=torch.int32, device=dev)
     tok_pp = [torch.empty(b_local, dtype=torch.int32, device=dev) for _ in range(2)]
     gstream = torch.cuda.Stream(device=dev)
     # the token all-gather through the library's C ABI (dp_allgather_tokens)
     gather = NcclTokenGather(shard, dev) if world > 1 else None
     base_it = [0]
-    # SHVS: the producer emits a penalty-free row summary with the logits
-    # (LM-head epilogue); the sampler corrects it for the penalty list, so a
-    # step streams only the hot prefix (+ tails of rejected rows).  The
-    # producer pass is timed separately below.
-    summaries = [plane.producer_summary(bf) for bf in bufs] if variant == "shvs" else None
 
     def sample_only(i):
         it = base_it[0] + i
@@ -568,11 +645,14 @@ def run_ours(args, cfg):
     kern_ms = _timed(kg) / args.kernel_steps
     producer_ms = None
     if variant == "shvs":
-        pg = _graph(lambda i: plane.producer_summary(bufs[i & 1]), args.kernel_steps)
-        torch.cuda.synchronize()
-        producer_ms = _timed(pg) / args.kernel_steps
+        producer_ms = {"separate_summary_pass": _graph_ms(lambda i: plane.producer_summary(bufs[i & 1]), 20),
+                       "note": "the timed step uses the summary the producer emitted with the logits"}
     d = sample_only(0)
     torch.cuda.synchronize()
+    # kernel-counted bytes loaded per row (dp_debug_t.bytes_touched), one untimed call
+    dm = plane.sample(bufs[0], 0, variant=variant, summary=summaries[0] if summaries else None,
+                      summary_raw=variant == "shvs", update=False, debug=True)
+    bytes_measured = float(dm.bytes_touched.double().mean().item())
     flags = d.flags.cpu().numpy()
     accept = float(np.mean((flags & 0x02) != 0)) if variant == "shvs" else None
     pen_len = plane.state.len.float().mean().item()
@@ -580,7 +660,7 @@ def run_ours(args, cfg):
     small = 8 * pen_len + 4 + 64 + 8 + 13                # penalty list, params, seq id, outputs
     if variant == "shvs":
         # algorithmic bytes: hot prefix (H) + tail on rejection + producer summary
-        h = args.hot
+        h = plane.hot.size
         bytes_per_row = h * esz + (1 - accept) * (v - h) * esz + 16 + small
     else:
         bytes_per_row = v * esz + small
@@ -654,7 +734,8 @@ def run_ours(args, cfg):
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic (SyntheticSource formula on device)",
             "config": {"workload": cfg["name"], "V": v, "B_per_gpu": b_local, "variant": variant,
-                       "hot_size": args.hot if variant == "shvs" else None,
+                       "hot_size": plane.hot.size if variant == "shvs" else None,
+                       "sizing": sizing_info,
                        "params": "5-way mix" if cfg.get("mix") else cfg["params"],
                        "l2": "inputs larger than L2 (2 x batch buffers alternate)",
                        "timing": "CUDA graph of the K steps" if graphed else "eager",
@@ -662,7 +743,10 @@ def run_ours(args, cfg):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                          "kernel": "dp_sample_full" if variant == "full" else "dp_sample_shvs",
-                         "kernel_ms": kern_ms, "bytes_per_row": bytes_per_row},
+                         "kernel_ms": kern_ms, "bytes_per_row": bytes_per_row,
+                         "bytes_per_row_measured": bytes_measured,
+                         "traffic_source": "profiles/traffic.json: ncu --set full dram__bytes_read.sum + "
+                                           "dram__bytes_write.sum of one launch of this kernel"},
             "producer_summary_ms": producer_ms,
             "shvs_accept": accept,
             "shvs": shvs,
@@ -684,8 +768,8 @@ def main():
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--kernel-steps", type=int, default=50)
-    ap.add_argument("--hot", type=int, default=4096,
-                    help="SHVS hot-set size (4,096: the measured optimum of tools/c3_sweep.py on this source)")
+    ap.add_argument("--hot", type=int, default=0,
+                    help="SHVS hot-set size; 0 (default): the sizing model's choice on this workload")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=None, choices=sorted(CONFIGS),
                     help="default: c2 on one GPU, c4 (B=8,192 split over the ranks, strong scaling) on N > 1")

@@ -253,17 +253,27 @@ DP_API int dp_ready_rows(const void* logits, int dtype, int64_t B, int64_t V, in
 
 /* SyntheticSource (service.py:429-467): base_by_id[V] (f64) + noise * Gumbel
  * keyed by (seed, DOMAIN_LOGITS, iteration, seq_ids[b], v), written as
- * fp32 or bf16 rows; perm (position -> id, may be NULL) writes hot-first rows. */
+ * fp32 or bf16 rows; perm (position -> id, may be NULL) writes hot-first rows.
+ * The producer-fused summary (make_shard_blocks, service.py:470-504): with
+ * row_max / total_expsum (and params, for tau) non-NULL the same pass also
+ * emits each row's penalty-free (max, Σ exp(x/tau - max)) of the values as
+ * written — dp_row_summary_raw's output, without re-reading the rows. */
 DP_API int dp_synth_logits(const double* base_by_id, double noise, uint64_t seed, uint64_t iteration,
                     const uint64_t* seq_ids, int64_t B, int64_t V, int64_t ld, const int32_t* perm,
-                    int dtype, void* out, void* stream);
+                    int dtype, void* out, const dp_params_t* params, double* row_max,
+                    double* total_expsum, void* stream);
 
 /* Batch hit-ratio curve (sizing.estimate_hit_ratio_curve, sizing.py:78-100):
- * out[b, g] = mass of the first grid[g] hot positions of the ready row. */
-DP_API int dp_hot_mass_curve(const void* logits_hotfirst, int dtype, int64_t B, int64_t V, int64_t ld,
+ * out[b, g] = ready mass of the first grid[g] positions of the curve's hot
+ * ordering / total_expsum.  inv_perm: token id -> curve position (penalty
+ * lookups).  col_of_pos (nullable): curve position -> column of `logits` when
+ * the rows are laid out in another order (the online sizing loop measures the
+ * master ordering on rows written for the current hot size); NULL: the rows
+ * are in curve order. */
+DP_API int dp_hot_mass_curve(const void* logits, int dtype, int64_t B, int64_t V, int64_t ld,
                       const double* row_max, const double* total_expsum,
                       const dp_params_t* params, const dp_penalty_t* pen_host,
-                      const int32_t* inv_perm, const int32_t* grid, int32_t n_grid,
+                      const int32_t* inv_perm, const int32_t* col_of_pos, const int32_t* grid, int32_t n_grid,
                       double* out, void* stream);
 
 /* DecisionBatch wire payload (transport.py:173-184) for B decisions: out =

@@ -105,13 +105,13 @@ _SIGS = {
     "dp_penalty_update": ([C.POINTER(Penalty), _P, _I64, _P, _P], C.c_int),
     "dp_penalty_reset": ([C.POINTER(Penalty), _I64, _P], C.c_int),
     "dp_ready_rows": ([_P, C.c_int, _I64, _I64, _I64, _P, C.POINTER(Penalty), _P, _P], C.c_int),
-    "dp_synth_logits": ([_P, _D, _U64, _U64, _P, _I64, _I64, _I64, _P, C.c_int, _P, _P], C.c_int),
+    "dp_synth_logits": ([_P, _D, _U64, _U64, _P, _I64, _I64, _I64, _P, C.c_int, _P, _P, _P, _P, _P], C.c_int),
     "dp_nccl_available": ([], C.c_int),
     "dp_nccl_unique_id": ([_P], C.c_int),
     "dp_nccl_comm_init": ([C.POINTER(C.c_void_p), _I32, _P, _I32], C.c_int),
     "dp_nccl_comm_destroy": ([_P], C.c_int),
     "dp_allgather_tokens": ([_P, _P, _I64, _P, _P], C.c_int),
-    "dp_hot_mass_curve": ([_P, C.c_int, _I64, _I64, _I64, _P, _P, _P, C.POINTER(Penalty), _P, _P, _I32,
+    "dp_hot_mass_curve": ([_P, C.c_int, _I64, _I64, _I64, _P, _P, _P, C.POINTER(Penalty), _P, _P, _P, _I32,
                            _P, _P], C.c_int),
 }
 

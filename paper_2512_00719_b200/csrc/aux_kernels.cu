@@ -96,22 +96,102 @@ __global__ void ready_rows_pen_kernel(const T* logits, int64_t V, int64_t ld, co
 // SyntheticSource.column (service.py:459-463): base + noise * Gumbel(u),
 // u keyed by (seed, DOMAIN_LOGITS, iteration, seq, v), clamped at 2^-60.
 template <typename T>
+DP_DEV float synth_value(const double* base, double noise, uint64_t h0, int64_t id, T* dst) {
+  double u = unit53(mix64(h0 ^ (uint64_t)id));
+  u = fmax(u, 8.673617379884035e-19);   // 2^-60
+  const double g = -log(-log(u));
+  const double z = base[id] + noise * g;
+  if constexpr (sizeof(T) == 4) {
+    *dst = (float)z;
+    return (float)z;
+  } else {
+    *dst = __float2bfloat16_rn((float)z);
+    return __bfloat162float(*dst);
+  }
+}
+
+template <typename T>
 __global__ void synth_kernel(const double* base, double noise, uint64_t seed, uint64_t iteration,
                              const uint64_t* seq_ids, int64_t V, int64_t ld, const int32_t* perm, T* out) {
   const int64_t row = blockIdx.y;
   const uint64_t h0 = mix64(hash_prefix(seed, kDomainLogits, iteration) ^ seq_ids[row]);
-  for (int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; pos < V; pos += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t id = perm ? (int64_t)perm[pos] : pos;
-    double u = unit53(mix64(h0 ^ (uint64_t)id));
-    u = fmax(u, 8.673617379884035e-19);   // 2^-60
-    const double g = -log(-log(u));
-    const double z = base[id] + noise * g;
-    if constexpr (sizeof(T) == 4) {
-      out[row * ld + pos] = (float)z;
-    } else {
-      out[row * ld + pos] = __float2bfloat16_rn((float)z);
+  for (int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; pos < V; pos += (int64_t)gridDim.x * blockDim.x)
+    synth_value<T>(base, noise, h0, perm ? (int64_t)perm[pos] : pos, out + row * ld + pos);
+}
+
+// The producer-fused summary (make_shard_blocks, service.py:470-504; paper:
+// "w can be pre-computed on GPUs when writing logits"): the same generator,
+// one 8-CTA cluster per row (rank r writes positions r*NT + tid + k*8*NT, so
+// the grid is as fine-grained as the plain generator's), every CTA folding
+// the values it writes (as rounded to T) into an online ExpSum; rank 0
+// combines the ranks' (max, sum) over DSMEM and emits the penalty-free
+// (row_max, total_expsum) of the row / tau — dp_row_summary_raw's output —
+// without re-reading the row.
+constexpr int kSynthCluster = 8;
+
+template <typename T, int NT>
+__global__ void __launch_bounds__(NT) synth_summary_kernel(const double* base, double noise, uint64_t seed,
+                                                           uint64_t iteration, const uint64_t* seq_ids, int64_t B,
+                                                           int64_t V, int64_t ld, const int32_t* perm, T* out,
+                                                           const dp_params_t* params, double* row_max,
+                                                           double* total) {
+  __shared__ float redf[NT / 32];
+  __shared__ double redd[NT / 32];
+  __shared__ float cta_m;
+  __shared__ double cta_s;
+  constexpr int C = kSynthCluster;
+  const uint32_t rank = cluster_ctarank();
+  const int64_t row = blockIdx.x / C;
+  const uint64_t h0 = mix64(hash_prefix(seed, kDomainLogits, iteration) ^ seq_ids[row]);
+  const double tau = params[row].temperature;
+  const float s2 = (float)(1.4426950408889634 / tau);
+  T* o = out + row * ld;
+  ExpSum acc;
+  for (int64_t p0 = (int64_t)rank * NT + threadIdx.x; p0 < V; p0 += 4 * C * NT) {
+    float x[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t pos = p0 + (int64_t)j * C * NT;
+      x[j] = pos < V ? synth_value<T>(base, noise, h0, perm ? (int64_t)perm[pos] : pos, o + pos) : -INFINITY;
     }
+#ifdef DP_SYNTH_NOSUM   // A-B build: the fused kernel's structure without the summary arithmetic
+    acc.m = fmaxf(acc.m, fmaxf(fmaxf(x[0], x[1]), fmaxf(x[2], x[3])));
+#else
+    acc.add(x, s2);
+#endif
   }
+  float m = warp_max(acc.m);
+  if ((threadIdx.x & 31u) == 0) redf[threadIdx.x >> 5] = m;
+  __syncthreads();
+  m = redf[0];
+#pragma unroll
+  for (int w = 1; w < NT / 32; ++w) m = fmaxf(m, redf[w]);
+  const double sr = warp_sum(acc.rel(m, s2));
+  if ((threadIdx.x & 31u) == 0) redd[threadIdx.x >> 5] = sr;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double S = 0.0;
+    for (int w = 0; w < NT / 32; ++w) S += redd[w];   // fixed order: deterministic
+    cta_m = m;
+    cta_s = S;
+  }
+  cluster_sync();   // every rank's (cta_m, cta_s) is visible cluster-wide
+  if (rank == 0 && threadIdx.x == 0) {
+    float rm[C];
+    double rs[C];
+    float M = -INFINITY;
+    for (int r = 0; r < C; ++r) {
+      rm[r] = __uint_as_float(ld_dsmem_u32(dsmem_addr(&cta_m, r)));
+      rs[r] = __longlong_as_double((long long)ld_dsmem_u64(dsmem_addr(&cta_s, r)));
+      M = fmaxf(M, rm[r]);
+    }
+    double S = 0.0;
+    for (int r = 0; r < C; ++r)
+      if (rm[r] != -INFINITY) S += rs[r] * exp2((double)(rm[r] - M) * (double)s2);
+    row_max[row] = M == -INFINITY ? -INFINITY : (tau != 1.0 ? __ddiv_rn((double)M, tau) : (double)M);
+    total[row] = S;
+  }
+  cluster_sync();   // rank 0 has read every peer's shared memory before anyone exits
 }
 
 // DecisionBatch wire payload (transport.py:173-184): u32 count, then per row
@@ -178,7 +258,27 @@ cudaError_t dp_launch_ready_rows(const void* logits, int dtype, int64_t B, int64
 }
 cudaError_t dp_launch_synth(const double* base, double noise, uint64_t seed, uint64_t iteration,
                             const uint64_t* seq_ids, int64_t B, int64_t V, int64_t ld, const int32_t* perm,
-                            int dtype, void* out, cudaStream_t st) {
+                            int dtype, void* out, const dp_params_t* params, double* row_max, double* total,
+                            cudaStream_t st) {
+  if (row_max) {
+    constexpr int NT = 256;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(B * kSynthCluster));
+    cfg.blockDim = dim3(NT);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kSynthCluster;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (dtype == DP_F32)
+      return cudaLaunchKernelEx(&cfg, synth_summary_kernel<float, NT>, base, noise, seed, iteration, seq_ids, B, V,
+                                ld, perm, (float*)out, params, row_max, total);
+    return cudaLaunchKernelEx(&cfg, synth_summary_kernel<__nv_bfloat16, NT>, base, noise, seed, iteration, seq_ids,
+                              B, V, ld, perm, (__nv_bfloat16*)out, params, row_max, total);
+  }
   dim3 g((unsigned)((V + 255) / 256 < 148 ? (V + 255) / 256 : 148), (unsigned)B);
   if (dtype == DP_F32)
     synth_kernel<float><<<g, 256, 0, st>>>(base, noise, seed, iteration, seq_ids, V, ld, perm, (float*)out);

@@ -17,8 +17,8 @@ cudaError_t launch_row_summary(const void* logits, int dtype, int64_t B, int64_t
                                double* row_max, double* total, cudaStream_t st);
 cudaError_t launch_hot_mass_curve(const void* logits, int dtype, int64_t B, int64_t V, int64_t ld,
                                   const double* row_max, const double* total, const dp_params_t* params,
-                                  const dp_penalty_t& pen, const int32_t* inv_perm, const int32_t* grid,
-                                  int32_t n_grid, double* out, cudaStream_t st);
+                                  const dp_penalty_t& pen, const int32_t* inv_perm, const int32_t* col_of_pos,
+                                  const int32_t* grid, int32_t n_grid, double* out, cudaStream_t st);
 }  // namespace dp
 
 cudaError_t dp_launch_uniforms(const dp_params_t*, const uint64_t*, int64_t, uint64_t, double*, cudaStream_t);
@@ -29,7 +29,8 @@ cudaError_t dp_launch_ready_rows(const void*, int, int64_t, int64_t, int64_t, co
 cudaError_t dp_launch_encode(const int32_t*, const double*, const uint8_t*, const uint64_t*, int64_t, uint8_t*,
                              cudaStream_t);
 cudaError_t dp_launch_synth(const double*, double, uint64_t, uint64_t, const uint64_t*, int64_t, int64_t,
-                            int64_t, const int32_t*, int, void*, cudaStream_t);
+                            int64_t, const int32_t*, int, void*, const dp_params_t*, double*, double*,
+                            cudaStream_t);
 
 // the ctypes mirrors (_native.py) and every caller rely on these layouts
 static_assert(sizeof(dp_params_t) == 64, "dp_params_t layout");
@@ -538,12 +539,17 @@ int dp_ready_rows(const void* logits, int dtype, int64_t B, int64_t V, int64_t l
 
 int dp_synth_logits(const double* base_by_id, double noise, uint64_t seed, uint64_t iteration,
                     const uint64_t* seq_ids, int64_t B, int64_t V, int64_t ld, const int32_t* perm, int dtype,
-                    void* out, void* stream) {
+                    void* out, const dp_params_t* params, double* row_max, double* total_expsum, void* stream) {
   if (!base_by_id || !seq_ids || !out) return fail(DP_ERR_ARG, "dp_synth_logits: null argument%s");
   if (dtype != DP_F32 && dtype != DP_BF16) return fail(DP_ERR_UNSUPPORTED, "dp_synth_logits: dtype%s");
+  if (B < 0 || V < 1 || ld < V) return fail(DP_ERR_ARG, "dp_synth_logits: bad shape%s");
+  const bool summ = row_max || total_expsum;
+  if (summ && (!row_max || !total_expsum || !params))
+    return fail(DP_ERR_ARG, "dp_synth_logits: the summary needs params, row_max and total_expsum%s");
   if (B == 0) return DP_OK;
   return cuda_status(dp_launch_synth(base_by_id, noise, seed, iteration, seq_ids, B, V, ld, perm, dtype, out,
-                                     (cudaStream_t)stream),
+                                     summ ? params : nullptr, summ ? row_max : nullptr,
+                                     summ ? total_expsum : nullptr, (cudaStream_t)stream),
                      "dp_synth_logits");
 }
 
@@ -557,13 +563,14 @@ int dp_encode_decisions(const int32_t* token, const double* logprob, const uint8
 
 int dp_hot_mass_curve(const void* logits, int dtype, int64_t B, int64_t V, int64_t ld, const double* row_max,
                       const double* total_expsum, const dp_params_t* params, const dp_penalty_t* pen_host,
-                      const int32_t* inv_perm, const int32_t* grid, int32_t n_grid, double* out, void* stream) {
+                      const int32_t* inv_perm, const int32_t* col_of_pos, const int32_t* grid, int32_t n_grid,
+                      double* out, void* stream) {
   if (!logits || !row_max || !total_expsum || !params || !grid || !out || n_grid < 1)
     return fail(DP_ERR_ARG, "dp_hot_mass_curve: null argument%s");
   if (!valid_pen(pen_host, V)) return fail(DP_ERR_ARG, "dp_hot_mass_curve: penalty state does not match V%s");
   if (B == 0) return DP_OK;
   return cuda_status(dp::launch_hot_mass_curve(logits, dtype, B, V, ld, row_max, total_expsum, params, *pen_host,
-                                               inv_perm, grid, n_grid, out, (cudaStream_t)stream),
+                                               inv_perm, col_of_pos, grid, n_grid, out, (cudaStream_t)stream),
                      "dp_hot_mass_curve");
 }
 

@@ -144,6 +144,40 @@ DP_DEV float ex2_fast(float x) {
   return y;
 }
 
+// Online (max, Σ exp) of raw values scaled by 1/tau, folded one small group
+// of elements at a time (a 16-byte vector or a few strided elements): one max
+// per group, the running sum rescaled (f64 exp2) only when the group raises
+// the maximum — rare after the first groups — and the group's terms
+// 2^((x - m) * log2e / tau) on the SFU, summed pairwise in f32 and added to
+// the f64 total once per group.  -inf entries (excluded / empty) contribute 0.
+struct ExpSum {
+  float m = -INFINITY;   // raw maximum seen so far
+  double s = 0.0;        // Σ 2^((x - m) s2)
+  template <int N>
+  DP_DEV void add(const float (&x)[N], float s2) {
+    float vm = x[0];
+#pragma unroll
+    for (int i = 1; i < N; ++i) vm = fmaxf(vm, x[i]);
+    if (vm > m) {
+      s = m == -INFINITY ? 0.0 : s * exp2((double)(m - vm) * (double)s2);
+      m = vm;
+    }
+    if (m == -INFINITY) return;
+    float e[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) e[i] = ex2_fast((x[i] - m) * s2);
+#pragma unroll
+    for (int st = 1; st < N; st <<= 1)
+#pragma unroll
+      for (int i = 0; i + st < N; i += 2 * st) e[i] += e[i + st];
+    s += (double)e[0];
+  }
+  // this state's sum relative to another maximum M >= m (f64)
+  DP_DEV double rel(float M, float s2) const {
+    return m == -INFINITY ? 0.0 : s * exp2((double)(m - M) * (double)s2);
+  }
+};
+
 // ---------------------------------------------------------------------------
 // warp helpers
 DP_DEV uint32_t lane_id() { return threadIdx.x & 31u; }

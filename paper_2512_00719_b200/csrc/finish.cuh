@@ -269,6 +269,7 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
     }
   };
 
+  if (t == 0) touch_bytes(a, row, (uint64_t)plen * sizeof(T));   // gathered penalty values
   // penalty entry e: (domain position, x, count), from the prefetch or memory
   auto pen_entry = [&](int32_t j, int32_t& pos, float& x, int32_t& c) {
     const int i = (j - (int32_t)t) / NT;
@@ -331,7 +332,6 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
         a.flags[row] = fl;
         if (a.dbg.alpha) a.dbg.alpha[row] = alpha;
         if (a.dbg.margin) a.dbg.margin[row] = fabs(u[1] - alpha);
-        if (a.dbg.bytes_touched) a.dbg.bytes_touched[row] = (uint64_t)n * sizeof(T);
         if (!(fl & DP_FLAG_DEGENERATE)) {
           a.reject_rows[atomicAdd(a.reject_count, 1)] = row;
         } else {
@@ -583,8 +583,6 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
       if (a.dbg.margin) a.dbg.margin[row] = MODE == kTail ? fmin(margin, a.dbg.margin[row]) : margin;
       if (a.dbg.kept) a.dbg.kept[row] = d.kept;
       if (MODE == kHot && a.dbg.alpha) a.dbg.alpha[row] = alpha;
-      if (a.dbg.bytes_touched)
-        a.dbg.bytes_touched[row] = (MODE == kTail ? a.dbg.bytes_touched[row] : 0ull) + (uint64_t)n * sizeof(T);
     }
     if (deferred && !fb && !degen && lane == 0) push_resum(a, row, s_dom);   // re-sum decides, then records
     if (!fb && !degen && !deferred) warp_record_token(a, row, pos_to_id(a, (int64_t)fpos[d.index] + lo));   // fused K5

@@ -241,11 +241,13 @@ __global__ void __launch_bounds__(kGenNT, 1) general_sample_kernel(SampleArgs a)
   }
   sync();
   const uint32_t np = g.ncol;
+  if (tid == 0) touch_bytes(a, row, (uint64_t)np * sizeof(T));   // gathered penalty values
   auto is_pen = [&](int64_t pos) -> bool { return np > 0 && ((bitmap[pos >> 5] >> (pos & 31)) & 1u); };
   auto val = [&](int64_t i) -> float { return Elem<T>::get(rowp, i); };
 
   // ---- pass A: max of unpenalised values
   float mx = -INFINITY;
+  if (tid == 0) touch_bytes(a, row, (uint64_t)n * sizeof(T));   // one more pass over the domain
   for_each_elem(rowp, n, tid, [&](int64_t i, float x) {
     if (!is_pen(i)) mx = fmaxf(mx, x);
   });
@@ -345,6 +347,7 @@ __global__ void __launch_bounds__(kGenNT, 1) general_sample_kernel(SampleArgs a)
   sync();
   unsigned long long wsum = 0, wminp = 0;
   uint32_t cminp = 0, cnp = 0;
+  if (tid == 0) touch_bytes(a, row, (uint64_t)n * sizeof(T));   // one more pass over the domain
   for_each_elem(rowp, n, tid, [&](int64_t i, float x) {
     if (is_pen(i)) return;
     const uint32_t b = bucket_of(x);
@@ -404,7 +407,6 @@ __global__ void __launch_bounds__(kGenNT, 1) general_sample_kernel(SampleArgs a)
         a.flags[row] = fl;
         if (a.dbg.alpha) a.dbg.alpha[row] = alpha;
         if (a.dbg.margin) a.dbg.margin[row] = fabs(u[1] - alpha);
-        if (a.dbg.bytes_touched) a.dbg.bytes_touched[row] = (uint64_t)n * sizeof(T);
         if (!(fl & DP_FLAG_DEGENERATE)) {
           a.reject_rows[atomicAdd(a.reject_count, 1)] = row;
         } else {
@@ -465,7 +467,8 @@ __global__ void __launch_bounds__(kGenNT, 1) general_sample_kernel(SampleArgs a)
       auto member = [&](unsigned long long k, uint32_t b) -> bool {
         return (use_bucket ? b == (uint32_t)bsel : true) && (k & pmask) == pref && in_range(k);
       };
-      for_each_elem(rowp, n, tid, [&](int64_t i, float x) {
+      if (tid == 0) touch_bytes(a, row, (uint64_t)n * sizeof(T));   // one more pass over the domain
+  for_each_elem(rowp, n, tid, [&](int64_t i, float x) {
         if (is_pen(i)) return;
         const uint32_t b = bucket_of(x);
         if (b != (uint32_t)bsel) return;
@@ -511,7 +514,8 @@ __global__ void __launch_bounds__(kGenNT, 1) general_sample_kernel(SampleArgs a)
     // collect the range: unpenalised + penalised members
     if (tid == 0) g.ncol = 0u;
     sync();
-    for_each_elem(rowp, n, tid, [&](int64_t i, float x) {
+    if (tid == 0) touch_bytes(a, row, (uint64_t)n * sizeof(T));   // one more pass over the domain
+  for_each_elem(rowp, n, tid, [&](int64_t i, float x) {
       if (is_pen(i)) return;
       if (bucket_of(x) != (uint32_t)bsel) return;
       const unsigned long long k = ekey(i, x);
@@ -666,8 +670,6 @@ __global__ void __launch_bounds__(kGenNT, 1) general_sample_kernel(SampleArgs a)
     if (a.dbg.margin) a.dbg.margin[row] = MODE == kTail ? fmin(margin, a.dbg.margin[row]) : margin;
     if (a.dbg.kept) a.dbg.kept[row] = (int32_t)kept;
     if (MODE == kHot && a.dbg.alpha) a.dbg.alpha[row] = alpha;
-    if (a.dbg.bytes_touched)
-      a.dbg.bytes_touched[row] = (MODE == kTail ? a.dbg.bytes_touched[row] : 0ull) + (uint64_t)n * sizeof(T);
     if (deferred) push_resum(a, row, sH);   // the exact re-sum decides, then records
     else thread_record_token(a, row, pos_to_id(a, gpos));   // fused K5
   }

@@ -307,10 +307,13 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
   // element >= threshold (one aggregated atomic per lane per batch).
   float t_lb = -INFINITY;
   uint32_t n_valid = 0;
+  uint64_t loaded = 0;   // tid 0: bytes this CTA streamed for the row (every pass)
   for (int pass_no = 0;; ++pass_no) {
   nscal_acc = 0u;
   for (int g = 0; g < spc; ++g) {
     if (g > 0 || (sharded && pass_no > 0)) set_segment(g);
+    if (tid == 0)
+      loaded += (uint64_t)(v_hi - v_lo) * 16u + (own_scal ? (uint64_t)(a0 + (n_seg - tail0)) * sizeof(T) : 0u);
     int32_t base = v_lo + (int32_t)warp * 32 * U;
     if (lane == 0) {   // the first kPrefetch chunks after the first batch -> L2
 #pragma unroll
@@ -471,6 +474,7 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
   }
 
   lapk(18);
+  if (tid == 0) touch_bytes(a, row, loaded);
   // ---- CTA-level exact top-kp
   {
     const uint32_t ns = min(ms.cnt, ccap) * EPV + (own_scal ? ms.nscal : 0u);

@@ -331,8 +331,10 @@ __global__ void __launch_bounds__(kMW * 32, kMWBlocks) warp_sample_kernel(Sample
       for (uint32_t mm = vm; mm; mm &= mm - 1u) wq[o++] = (uint32_t)(base + (J0 + __ffs(mm) - 1) * stride);
       qn += tot;
     };
+    int npass = 0;
     for (int pass_no = 0;; ++pass_no) {
       const bool first = pass_no == 0;
+      npass = pass_no + 1;
       if (warp == 0) {   // scalar head / tail elements (at most 2*EPV-2)
         const int32_t hi_i = (int32_t)lane, ti = tail0 + (int32_t)lane;
         const bool hv = hi_i < a0, tv = ti < n;
@@ -378,6 +380,11 @@ __global__ void __launch_bounds__(kMW * 32, kMWBlocks) warp_sample_kernel(Sample
       const double s = warp_sum(sh);
       if (lane == 0) S.sh[warp] = s;
     }
+    // every pass loads the row's vectors once plus its scalar head / tail;
+    // the penalty values are gathered once below
+    if (threadIdx.x == 0)
+      touch_bytes(a, row, (uint64_t)npass * ((uint64_t)nvec * 16u + (uint64_t)(a0 + (n - tail0)) * sizeof(T)) +
+                              (uint64_t)plen * sizeof(T));
     __syncthreads();
     lap(5);
     // ---- penalty list (after the stream: the row and the id maps are L2-hot;
@@ -461,7 +468,6 @@ __global__ void __launch_bounds__(kMW * 32, kMWBlocks) warp_sample_kernel(Sample
           a.flags[row] = fl;
           if (a.dbg.alpha) a.dbg.alpha[row] = alpha;
           if (a.dbg.margin) a.dbg.margin[row] = fabs(u[1] - alpha);
-          if (a.dbg.bytes_touched) a.dbg.bytes_touched[row] = (uint64_t)n * sizeof(T);
           if (!(fl & DP_FLAG_DEGENERATE)) {
             a.reject_rows[atomicAdd(a.reject_count, 1)] = row;
           } else {
@@ -582,7 +588,6 @@ __global__ void __launch_bounds__(kMW * 32, kMWBlocks) warp_sample_kernel(Sample
       if (a.dbg.margin) a.dbg.margin[row] = margin;
       if (a.dbg.kept) a.dbg.kept[row] = d.kept;
       if (MODE == kHot && a.dbg.alpha) a.dbg.alpha[row] = alpha;
-      if (a.dbg.bytes_touched) a.dbg.bytes_touched[row] = (uint64_t)n * sizeof(T);
       if (a.dbg.stats) atomicAdd((unsigned long long*)&a.dbg.stats[0], 1ull);
     }
     if (deferred) {

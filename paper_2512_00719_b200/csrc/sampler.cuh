@@ -73,6 +73,15 @@ DP_DEV const T* domain_row(const SampleArgs& a, int row, int mode) {
   return reinterpret_cast<const T*>(a.logits) + (int64_t)row * a.ld + dom_lo(a, mode);
 }
 // raw logit at an absolute row position (either storage)
+// VisitCounter (instrument.py:6-33) on the device: bytes this launch loaded
+// for `row` — every streaming pass (re-streams included), scalar head / tail
+// elements and gathered penalty values — accumulated per row across the
+// kernels of one call (the host zeroes the counters before a debug call).
+DP_DEV void touch_bytes(const SampleArgs& a, int row, uint64_t bytes) {
+  if (a.dbg.bytes_touched && bytes)
+    atomicAdd(reinterpret_cast<unsigned long long*>(a.dbg.bytes_touched + row), (unsigned long long)bytes);
+}
+
 template <typename T>
 DP_DEV float row_value(const SampleArgs& a, int row, int64_t pos) {
   if (a.tail_logits && pos >= a.H)

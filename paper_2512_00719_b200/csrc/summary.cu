@@ -2,9 +2,10 @@
 //
 // K2 is make_shard_blocks' per-row (row_max, total_expsum) over the penalized,
 // temperature-scaled row (service.py:470-504, shvs.row_summary shvs.py:157-168):
-// one streaming pass with a per-thread online (max, sum) pair; penalized ids
-// are excluded from the stream through a shared-memory bitmap and added back
-// exactly in f64, so heavy penalties cannot cancel catastrophically.
+// one streaming pass with a per-thread online (max, sum) pair (ExpSum,
+// common.cuh); penalized ids are excluded from the stream through a
+// shared-memory bitmap and added back exactly in f64, so heavy penalties
+// cannot cancel catastrophically.
 #include "sampler.cuh"
 
 namespace dp {
@@ -40,11 +41,16 @@ DP_DEV float block_max_f32(float v, float* red) {
   return v;
 }
 
-template <typename T, int NT, int U>
-__global__ void __launch_bounds__(NT) row_summary_kernel(const T* logits, int64_t V, int64_t ld,
-                                                         const dp_params_t* params, dp_penalty_t pen,
-                                                         const int32_t* inv_perm, double* row_max,
-                                                         double* total) {
+// One CTA per row, 16-byte streaming loads (U per thread in flight), the
+// online ExpSum per vector (one max + compare, SFU exp2 terms centred on the
+// running maximum, one f64 add per vector).  PEN: penalized positions are
+// masked to -inf through the shared bitmap (one funnel shift per vector) and
+// added back exactly in f64 after the stream.
+template <typename T, int NT, int U, bool PEN>
+__global__ void __launch_bounds__(NT, 2048 / NT / 2) row_summary_kernel(const T* logits, int64_t V, int64_t ld,
+                                                                      const dp_params_t* params, dp_penalty_t pen,
+                                                                      const int32_t* inv_perm, double* row_max,
+                                                                      double* total) {
   constexpr int EPV = Elem<T>::kPerVec;
   extern __shared__ __align__(16) uint8_t smem[];
   double* redd = reinterpret_cast<double*>(smem);
@@ -53,83 +59,89 @@ __global__ void __launch_bounds__(NT) row_summary_kernel(const T* logits, int64_
   const int64_t row = blockIdx.x;
   const dp_params_t p = params[row];
   const T* x = logits + row * ld;
-  const int32_t plen = (penalties_neutral(p) || pen.len == nullptr) ? 0 : pen.len[row];
+  const int32_t plen = (!PEN || penalties_neutral(p) || pen.len == nullptr) ? 0 : pen.len[row];
   const int32_t* pids = pen.ids + row * pen.cap;
   const int32_t* pcnt = pen.out_count + row * pen.cap;
-  const uint32_t words = plen > 0 ? (uint32_t)((V + 31) / 32) : 0u;
-  for (uint32_t i = threadIdx.x; i < words; i += NT) bitmap[i] = 0u;
-  __syncthreads();
-  for (int32_t j = threadIdx.x; j < plen; j += NT) {
-    const int64_t pos = inv_perm ? inv_perm[pids[j]] : pids[j];
-    atomicOr(&bitmap[pos >> 5], 1u << (pos & 31));
-  }
-  __syncthreads();
-  const float inv_tau = (float)(1.0 / p.temperature);
-  float m = -INFINITY;
-  double s = 0.0;
-  auto take = [&](float v, int64_t pos, bool valid) {
-    if (!valid) return;
-    if (plen > 0 && ((bitmap[pos >> 5] >> (pos & 31)) & 1u)) return;
-    if (v > m) {
-      s = (m == -INFINITY) ? 0.0 : s * (double)expf((m - v) * inv_tau);
-      m = v;
-    }
-    s += (double)expf((v - m) * inv_tau);
-  };
   const uintptr_t addr = reinterpret_cast<uintptr_t>(x);
-  const int64_t a0 = min64(V, (int64_t)(((16u - (addr & 15u)) & 15u) / sizeof(T)));
-  const int64_t nvec = (V - a0) / EPV;
-  const int64_t tail0 = a0 + nvec * EPV;
-  if (threadIdx.x < 32) {
-    const int64_t i = threadIdx.x, ti = tail0 + threadIdx.x;
-    take(i < a0 ? Elem<T>::get(x, i) : 0.f, i, i < a0);
-    take(ti < V ? Elem<T>::get(x, ti) : 0.f, ti, ti < V);
+  const int32_t a0 = (int32_t)min64(V, (int64_t)(((16u - (addr & 15u)) & 15u) / sizeof(T)));
+  const int32_t nvec = (int32_t)((V - a0) / EPV);
+  const int32_t tail0 = a0 + nvec * EPV;
+  if (PEN) {
+    const uint32_t words = (uint32_t)((V + 31) / 32) + 1u;   // +1: funnel-shift window
+    for (uint32_t i = threadIdx.x; i < words; i += NT) bitmap[i] = 0u;
+    __syncthreads();
+    for (int32_t j = threadIdx.x; j < plen; j += NT) {
+      const int64_t pos = inv_perm ? inv_perm[pids[j]] : pids[j];
+      atomicOr(&bitmap[pos >> 5], 1u << (pos & 31));
+    }
+    __syncthreads();
+  }
+  const float s2 = (float)(1.4426950408889634 / p.temperature);
+  auto masked = [&](float v, int64_t pos) -> float {
+    return (PEN && plen > 0 && ((bitmap[pos >> 5] >> (pos & 31)) & 1u)) ? -INFINITY : v;
+  };
+  ExpSum acc;
+  if (threadIdx.x < 32) {   // scalar head / tail elements
+    const int32_t i = threadIdx.x, ti = tail0 + threadIdx.x;
+    float h[2] = {i < a0 ? masked(Elem<T>::get(x, i), i) : -INFINITY,
+                  ti < V ? masked(Elem<T>::get(x, ti), ti) : -INFINITY};
+    acc.add(h, s2);
   }
   const uint4* vp = reinterpret_cast<const uint4*>(x + a0);
-  for (int64_t base = threadIdx.x; base < nvec; base += (int64_t)NT * U) {
+  auto fold = [&](const uint4& vv, int32_t idx) {
+    float e[EPV];
+#pragma unroll
+    for (int i = 0; i < EPV; ++i) e[i] = vec_elem<T>(vv, i);
+    if (PEN && plen > 0) {
+      const uint32_t p0 = (uint32_t)(a0 + idx * EPV);
+      const uint32_t pm = __funnelshift_r(bitmap[p0 >> 5], bitmap[(p0 >> 5) + 1], p0 & 31u);
+#pragma unroll
+      for (int i = 0; i < EPV; ++i) if ((pm >> i) & 1u) e[i] = -INFINITY;
+    }
+    acc.add(e, s2);
+  };
+  int32_t base = threadIdx.x;
+  for (; base + (U - 1) * NT < nvec; base += NT * U) {   // full batches: unpredicated loads
     uint4 v[U];
 #pragma unroll
-    for (int j = 0; j < U; ++j) {
-      const int64_t idx = base + (int64_t)j * NT;
-      v[j] = idx < nvec ? ld_stream16(vp + idx) : make_uint4(0u, 0u, 0u, 0u);
-    }
+    for (int j = 0; j < U; ++j) v[j] = ld_stream16(vp + base + j * NT);
 #pragma unroll
-    for (int j = 0; j < U; ++j) {
-      const int64_t idx = base + (int64_t)j * NT;
-#pragma unroll
-      for (int e = 0; e < EPV; ++e) take(vec_elem<T>(v[j], e), a0 + idx * EPV + e, idx < nvec);
-    }
+    for (int j = 0; j < U; ++j) fold(v[j], base + j * NT);
   }
-  // combine thread states: global raw max, then rescale partial sums (f64)
-  const float mnp = block_max_f32<NT>(m, redf);
-  double sc = 0.0;
-  if (m != -INFINITY) sc = s * exp(((double)m - (double)mnp) * (double)inv_tau);
-  const double snp = block_sum_f64<NT>(sc, redd);
+  for (int32_t idx = base; idx < nvec; idx += NT) fold(ld_stream16(vp + idx), idx);
+  // combine thread states: raw maximum, then every partial sum rescaled to it
+  const float mnp = block_max_f32<NT>(acc.m, redf);
+  const double snp = block_sum_f64<NT>(acc.rel(mnp, s2), redd);
   // penalized ids, exact f64 (penalty.py:66-78)
-  double rmax_pen = -INFINITY;
-  for (int32_t j = threadIdx.x; j < plen; j += NT) {
-    const int64_t pos = inv_perm ? inv_perm[pids[j]] : pids[j];
-    rmax_pen = fmax(rmax_pen, ready_penalized(Elem<T>::get(x, pos), pcnt[j], p));
+  double rpen = -INFINITY, sp = 0.0;
+  if (PEN) {
+    double rmax_pen = -INFINITY;
+    for (int32_t j = threadIdx.x; j < plen; j += NT) {
+      const int64_t pos = inv_perm ? inv_perm[pids[j]] : pids[j];
+      rmax_pen = fmax(rmax_pen, ready_penalized(Elem<T>::get(x, pos), pcnt[j], p));
+    }
+    rmax_pen = warp_max(rmax_pen);
+    if ((threadIdx.x & 31u) == 0) redd[threadIdx.x >> 5] = rmax_pen;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double mm = redd[0];
+      for (int w = 1; w < NT / 32; ++w) mm = fmax(mm, redd[w]);
+      redd[33] = mm;
+    }
+    __syncthreads();
+    rpen = redd[33];
+    __syncthreads();
   }
-  rmax_pen = warp_max(rmax_pen);
-  if ((threadIdx.x & 31u) == 0) redd[threadIdx.x >> 5] = rmax_pen;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double mm = redd[0];
-    for (int w = 1; w < NT / 32; ++w) mm = fmax(mm, redd[w]);
-    redd[33] = mm;
-  }
-  __syncthreads();
-  const double rpen = redd[33];
-  __syncthreads();
   const double rnp = mnp == -INFINITY ? -INFINITY : ready_plain(mnp, p);
   const double M = fmax(rnp, rpen);
-  double spen = 0.0;
-  for (int32_t j = threadIdx.x; j < plen; j += NT) {
-    const int64_t pos = inv_perm ? inv_perm[pids[j]] : pids[j];
-    spen += exp(ready_penalized(Elem<T>::get(x, pos), pcnt[j], p) - M);
+  if (PEN) {
+    double spen = 0.0;
+    for (int32_t j = threadIdx.x; j < plen; j += NT) {
+      const int64_t pos = inv_perm ? inv_perm[pids[j]] : pids[j];
+      spen += exp(ready_penalized(Elem<T>::get(x, pos), pcnt[j], p) - M);
+    }
+    sp = block_sum_f64<NT>(spen, redd);
   }
-  const double sp = block_sum_f64<NT>(spen, redd);
   if (threadIdx.x == 0) {
     row_max[row] = M;
     total[row] = (rnp == -INFINITY ? 0.0 : snp * exp(rnp - M)) + sp;
@@ -141,8 +153,8 @@ template <typename T, int NT>
 __global__ void __launch_bounds__(NT) hot_mass_curve_kernel(const T* logits, int64_t V, int64_t ld,
                                                             const double* row_max, const double* total,
                                                             const dp_params_t* params, dp_penalty_t pen,
-                                                            const int32_t* inv_perm, const int32_t* grid,
-                                                            int32_t n_grid, double* out) {
+                                                            const int32_t* inv_perm, const int32_t* col_of_pos,
+                                                            const int32_t* grid, int32_t n_grid, double* out) {
   extern __shared__ __align__(16) uint8_t smem[];
   double* redd = reinterpret_cast<double*>(smem);
   uint32_t* bitmap = reinterpret_cast<uint32_t*>(smem + 40 * 8);
@@ -172,12 +184,13 @@ __global__ void __launch_bounds__(NT) hot_mass_curve_kernel(const T* logits, int
     double s = 0.0;
     for (int64_t pos = lo + threadIdx.x; pos < hi; pos += NT) {
       if (plen > 0 && ((bitmap[pos >> 5] >> (pos & 31)) & 1u)) continue;
-      const float v = Elem<T>::get(x, pos);
+      const float v = Elem<T>::get(x, col_of_pos ? (int64_t)col_of_pos[pos] : pos);
       s += (double)expf(((v - c_hi) - c_lo) * inv_tau);
     }
     for (int32_t j = threadIdx.x; j < plen; j += NT) {
       const int64_t pos = inv_perm ? inv_perm[pids[j]] : pids[j];
-      if (pos >= lo && pos < hi) s += exp(ready_penalized(Elem<T>::get(x, pos), pcnt[j], p) - M);
+      if (pos >= lo && pos < hi)
+        s += exp(ready_penalized(Elem<T>::get(x, col_of_pos ? (int64_t)col_of_pos[pos] : pos), pcnt[j], p) - M);
     }
     acc += block_sum_f64<NT>(s, redd);
     if (threadIdx.x == 0) out[row * n_grid + g] = S > 0.0 ? fmin(acc / S, 1.0) : 0.0;
@@ -230,7 +243,7 @@ __global__ void __launch_bounds__(NT) resum_kernel(SampleArgs a) {
       const double alpha = ok ? fmin(sH / S, 1.0) : 1.0;
       const bool near = fabs(u[1] - alpha) < kBoundaryEps;
       if (a.dbg.alpha) a.dbg.alpha[row] = alpha;
-      if (a.dbg.bytes_touched) a.dbg.bytes_touched[row] += (uint64_t)a.V * sizeof(T);
+      touch_bytes(a, row, (uint64_t)(a.V + plen) * sizeof(T));   // the whole row + the penalty values
       if (a.dbg.stats) atomicAdd((unsigned long long*)&a.dbg.stats[2], 1ull);
       if (!ok) {
         a.token[row] = -1;
@@ -268,39 +281,47 @@ cudaError_t launch_resum(const SampleArgs& a, int dtype, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+template <typename T, bool PEN>
+static void row_summary_t(const void* logits, int64_t B, int64_t V, int64_t ld, const dp_params_t* params,
+                          const dp_penalty_t& pen, const int32_t* inv_perm, double* row_max, double* total,
+                          cudaStream_t st) {
+  constexpr int NT = 256, U = 4;
+  const size_t smem = 40 * 8 + 40 * 4 + (PEN ? (size_t)((V + 31) / 32 + 1) * 4 : 0);
+  auto k = row_summary_kernel<T, NT, U, PEN>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k<<<(unsigned)B, NT, smem, st>>>((const T*)logits, V, ld, params, pen, inv_perm, row_max, total);
+}
+
 cudaError_t launch_row_summary(const void* logits, int dtype, int64_t B, int64_t V, int64_t ld,
                                const dp_params_t* params, const dp_penalty_t& pen, const int32_t* inv_perm,
                                double* row_max, double* total, cudaStream_t st) {
-  constexpr int NT = 512, U = 4;
-  const size_t smem = 40 * 8 + 40 * 4 + (pen.len ? (size_t)((V + 31) / 32) * 4 : 0);
+  const bool pen_on = pen.len != nullptr;   // dp_row_summary_raw passes no penalty state
   if (dtype == DP_F32) {
-    auto k = row_summary_kernel<float, NT, U>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k<<<(unsigned)B, NT, smem, st>>>((const float*)logits, V, ld, params, pen, inv_perm, row_max, total);
+    if (pen_on) row_summary_t<float, true>(logits, B, V, ld, params, pen, inv_perm, row_max, total, st);
+    else row_summary_t<float, false>(logits, B, V, ld, params, pen, inv_perm, row_max, total, st);
   } else {
-    auto k = row_summary_kernel<__nv_bfloat16, NT, U>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k<<<(unsigned)B, NT, smem, st>>>((const __nv_bfloat16*)logits, V, ld, params, pen, inv_perm, row_max, total);
+    if (pen_on) row_summary_t<__nv_bfloat16, true>(logits, B, V, ld, params, pen, inv_perm, row_max, total, st);
+    else row_summary_t<__nv_bfloat16, false>(logits, B, V, ld, params, pen, inv_perm, row_max, total, st);
   }
   return cudaGetLastError();
 }
 
 cudaError_t launch_hot_mass_curve(const void* logits, int dtype, int64_t B, int64_t V, int64_t ld,
                                   const double* row_max, const double* total, const dp_params_t* params,
-                                  const dp_penalty_t& pen, const int32_t* inv_perm, const int32_t* grid,
-                                  int32_t n_grid, double* out, cudaStream_t st) {
+                                  const dp_penalty_t& pen, const int32_t* inv_perm, const int32_t* col_of_pos,
+                                  const int32_t* grid, int32_t n_grid, double* out, cudaStream_t st) {
   constexpr int NT = 256;
   const size_t smem = 40 * 8 + (size_t)((V + 31) / 32) * 4;
   if (dtype == DP_F32) {
     auto k = hot_mass_curve_kernel<float, NT>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k<<<(unsigned)B, NT, smem, st>>>((const float*)logits, V, ld, row_max, total, params, pen, inv_perm, grid,
-                                     n_grid, out);
+    k<<<(unsigned)B, NT, smem, st>>>((const float*)logits, V, ld, row_max, total, params, pen, inv_perm,
+                                     col_of_pos, grid, n_grid, out);
   } else {
     auto k = hot_mass_curve_kernel<__nv_bfloat16, NT>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k<<<(unsigned)B, NT, smem, st>>>((const __nv_bfloat16*)logits, V, ld, row_max, total, params, pen, inv_perm,
-                                     grid, n_grid, out);
+                                     col_of_pos, grid, n_grid, out);
   }
   return cudaGetLastError();
 }

@@ -72,7 +72,7 @@ class Decisions:
     alpha: "object" = None   # float64 (SHVS hot mass)
     margin: "object" = None  # float64 (closest decision-boundary distance)
     kept: "object" = None
-    bytes_touched: "object" = None
+    bytes_touched: "object" = None   # int64: bytes the call's kernels loaded per row (debug)
     topk_ids: "object" = None
     topk_ready: "object" = None
     stats: "object" = None   # int64[24] launch counters (see dp_debug_t.stats)
@@ -174,6 +174,7 @@ class DecisionPlane:
     def _debug_struct(self, d: Decisions, topk_stride: int, debug: bool) -> N.Debug:
         if not debug:
             return N.Debug(None, None, 0, 0, None, None, d.alpha.data_ptr(), None, None)
+        d.bytes_touched.zero_()   # the kernels of one call accumulate into it (VisitCounter)
         return N.Debug(_ptr(d.topk_ids).value, _ptr(d.topk_ready).value, topk_stride, 0, d.margin.data_ptr(),
                        d.kept.data_ptr(), d.alpha.data_ptr(), d.bytes_touched.data_ptr(), d.stats.data_ptr())
 
@@ -347,10 +348,15 @@ class DecisionPlane:
         tail = logits_host[:, h:]
         return self.sample_split(staging, tail, iteration, (rmax, tot), update=update, summary_raw=summary_raw)
 
-    def hot_mass_curve(self, logits_hotfirst, grid, summary=None):
+    def hot_mass_curve(self, logits_hotfirst, grid, summary=None, order: HotVocab | None = None):
         """Per-row hot mass alpha(H) at every grid size H (ready mass of the
         first H hot positions / total), [B, G] f64 on device — the batched
-        GPU form of sizing.estimate_hit_ratio_curve (sizing.py:78-100)."""
+        GPU form of sizing.estimate_hit_ratio_curve (sizing.py:78-100).
+
+        The curve follows the plane's hot ordering, or `order` (e.g. the
+        master ordering of the online sizing loop, a longer ordering than the
+        current hot set): the rows stay in the plane's current hot-first
+        layout and are read through the position map."""
         import torch
 
         if self.hot is None:
@@ -361,14 +367,20 @@ class DecisionPlane:
             raise ValueError(f"grid sizes must lie in [1, {self.vocab_size}]")
         with torch.cuda.device(self.device):
             perm, inv = self.hot.device_maps(self.device)
+            col = None
+            if order is not None and not np.array_equal(order.perm, self.hot.perm):
+                _, oinv = order.device_maps(self.device)
+                col = inv.index_select(0, order.device_maps(self.device)[0].long())   # curve pos -> column
+                inv = oinv
             if summary is None:
-                summary = self.row_summary(logits_hotfirst, inv_perm=inv)
+                summary = self.row_summary(logits_hotfirst, inv_perm=self.hot.device_maps(self.device)[1])
             rmax, tot = summary
             gd = torch.tensor(g, dtype=torch.int32, device=self.device)
             out = torch.empty((self.batch, len(g)), dtype=torch.float64, device=self.device)
             N.call("dp_hot_mass_curve", _ptr(logits_hotfirst), _dtype_code(logits_hotfirst), self.batch,
                    self.vocab_size, logits_hotfirst.stride(0), _ptr(rmax), _ptr(tot), _ptr(self._params_dev),
-                   C.byref(self.state.native), _ptr(inv), _ptr(gd), len(g), _ptr(out), _stream(self.device))
+                   C.byref(self.state.native), _ptr(inv), _ptr(col), _ptr(gd), len(g), _ptr(out),
+                   _stream(self.device))
         return out
 
     def row_summary(self, logits, inv_perm=None):

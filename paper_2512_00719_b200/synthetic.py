@@ -61,19 +61,36 @@ class SyntheticSource:
     def hot_ordering(self) -> np.ndarray:
         return self.rank_to_token
 
-    def generate(self, iteration: int, seq_ids, dtype=None, perm=None, out=None):
+    def generate(self, iteration: int, seq_ids, dtype=None, perm=None, out=None, summary_params=None,
+                 summary_out=None):
         """[B, V] logits for (iteration, seq_ids); perm (int32 device tensor,
-        position -> id) writes hot-first rows."""
+        position -> id) writes hot-first rows.  With `summary_params` (the
+        plane's device dp_params_t array, for tau) the same pass also emits
+        the producer's penalty-free row summary and the call returns
+        (logits, (row_max, total_expsum)) — make_shard_blocks' contract
+        (service.py:470-504) with the summary computed while the logits are
+        written (into `summary_out` = (row_max, total_expsum) f64 [B] when
+        given)."""
         import torch
 
         dtype = torch.float32 if dtype is None else dtype
-        seq = torch.as_tensor(np.asarray(seq_ids, dtype=np.uint64).view(np.int64), device=self.device)
+        if isinstance(seq_ids, torch.Tensor) and seq_ids.is_cuda:   # device ids: capturable in a CUDA graph
+            seq = seq_ids
+        else:
+            seq = torch.as_tensor(np.asarray(seq_ids, dtype=np.uint64).view(np.int64), device=self.device)
         bsz = seq.shape[0]
         if out is None:
             out = torch.empty((bsz, self.vocab_size), dtype=dtype, device=self.device)
         code = N.DP_F32 if out.dtype == torch.float32 else N.DP_BF16
+        rmax = tot = None
+        if summary_params is not None and summary_out is not None:
+            rmax, tot = summary_out
+        elif summary_params is not None:
+            rmax = torch.empty(bsz, dtype=torch.float64, device=self.device)
+            tot = torch.empty(bsz, dtype=torch.float64, device=self.device)
+        ptr = lambda t: C.c_void_p(0 if t is None else t.data_ptr())   # noqa: E731
         N.call("dp_synth_logits", C.c_void_p(self._base.data_ptr()), self.noise, self.seed, int(iteration),
-               C.c_void_p(seq.data_ptr()), bsz, self.vocab_size, out.stride(0),
-               C.c_void_p(0 if perm is None else perm.data_ptr()), code, C.c_void_p(out.data_ptr()),
-               C.c_void_p(torch.cuda.current_stream().cuda_stream))
-        return out
+               C.c_void_p(seq.data_ptr()), bsz, self.vocab_size, out.stride(0), ptr(perm), code,
+               C.c_void_p(out.data_ptr()), ptr(summary_params), ptr(rmax), ptr(tot),
+               C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream))
+        return out if summary_params is None else (out, (rmax, tot))

@@ -717,9 +717,13 @@ def _big_batch_parity(torch, v, bsz, bf16, mix, variant, hot_size, check_every, 
     exempt, rejected = [], 0
     dt = torch.bfloat16 if bf16 else torch.float32
     for it in range(iters):
-        x = src.generate(it, range(bsz), dtype=dt, perm=perm)
+        if raw == "synth":   # the producer-fused summary, emitted while the logits are written
+            x, summ = src.generate(it, range(bsz), dtype=dt, perm=perm, summary_params=plane.params_dev)
+        else:
+            x = src.generate(it, range(bsz), dtype=dt, perm=perm)
         if variant == "shvs":
-            summ = plane.producer_summary(x) if raw else None
+            if raw != "synth":
+                summ = plane.producer_summary(x) if raw else None
             d = plane.sample(x, it, variant="shvs", summary=summ, summary_raw=raw and summ is not None)
         else:
             d = plane.sample(x, it)
@@ -761,10 +765,50 @@ def test_c4_full_batch_matches_oracle(torch_cuda):
     torch.cuda.empty_cache()
 
 
-@pytest.mark.parametrize("raw", [False, True])
+@pytest.mark.parametrize("raw", [False, True, "synth"])
 def test_c2_shvs_bench_config_matches_oracle(torch_cuda, raw):
-    """The bench's SHVS line: C2 at full size, H=4,096 hot head."""
+    """The bench's SHVS line: C2 at full size, H=4,096 hot head; the summary
+    exact and penalized (False), the producer's raw one from a separate pass
+    (True), or emitted by the producer while writing the logits ("synth")."""
     _big_batch_parity(torch_cuda, 152064, 1024, False, False, "shvs", 4096, 8, raw=raw)
+
+
+def test_c5_mix_shvs_with_producer_fused_summary(torch_cuda):
+    """C5 row mix (bf16, 5 kinds, penalties alternating) at V=152,064, SHVS
+    with the summary the producer emits while writing the bf16 rows."""
+    _big_batch_parity(torch_cuda, 152064, 2048, True, True, "shvs", 4096, 8, raw="synth")
+
+
+@pytest.mark.parametrize("bf16", [False, True])
+def test_producer_fused_summary_matches_separate_pass(torch_cuda, bf16):
+    """dp_synth_logits with the fused summary writes the same logits as the
+    plain generator and a summary equal to dp_row_summary_raw's (relative
+    1e-6: both sum SFU exp2 terms, in different orders) and to the f64 oracle
+    of the written values."""
+    torch = torch_cuda
+    from paper_2512_00719_b200 import DecisionPlane, HotVocab, SamplingParams
+    from paper_2512_00719_b200.synthetic import SyntheticSource
+
+    v, bsz = 152064, 96
+    taus = [0.5, 0.8, 1.0, 1.7]
+    plane = DecisionPlane(v, [SamplingParams(temperature=taus[b % 4], seed=b) for b in range(bsz)])
+    src = SyntheticSource(v, device="cuda")
+    hot = HotVocab(v, src.hot_ordering()[:4096])
+    perm = hot.device_maps(plane.device)[0]
+    dt = torch.bfloat16 if bf16 else torch.float32
+    for pm in (None, perm):
+        x0 = src.generate(5, range(bsz), dtype=dt, perm=pm)
+        x1, (m1, s1) = src.generate(5, range(bsz), dtype=dt, perm=pm, summary_params=plane.params_dev)
+        assert torch.equal(x0, x1)
+        m0, s0 = plane.producer_summary(x1)
+        np.testing.assert_allclose(m1.cpu().numpy(), m0.cpu().numpy(), rtol=0, atol=0)
+        np.testing.assert_allclose(s1.cpu().numpy(), s0.cpu().numpy(), rtol=1e-6)
+        xh = x1.float().cpu().numpy().astype(np.float64)
+        for b in range(0, bsz, 7):
+            r = xh[b] / taus[b % 4]
+            mx = r.max()
+            assert m1[b].item() == mx
+            np.testing.assert_allclose(s1[b].item(), np.exp(r - mx).sum(), rtol=1e-6)
 
 
 # ---------------------------------------------------------------------------
