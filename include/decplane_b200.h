@@ -122,6 +122,11 @@ typedef struct {
  * goes through the exact re-sum (normally only the ones the cancelling
  * correction cannot decide) */
 #define DP_PLAN_FORCE_RESUM 0x1
+/* dp_sample_full: keep the one-CTA-per-row top-k kernel even when the batch
+ * spans several waves (A-B tests of the persistent warp-specialised K1p) */
+#define DP_PLAN_NO_PERSIST 0x2
+/* dp_sample_full: use K1p whenever its rows allow (tests) */
+#define DP_PLAN_FORCE_PERSIST 0x4
 
 typedef struct {
   int32_t max_top_k;

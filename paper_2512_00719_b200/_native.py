@@ -23,6 +23,8 @@ FLAG_REJECTED = 0x08
 FLAG_PEN_OVERFLOW = 0x40
 FLAG_DEGENERATE = 0x80
 PLAN_FORCE_RESUM = 0x1
+PLAN_NO_PERSIST = 0x2
+PLAN_FORCE_PERSIST = 0x4
 
 EXPORTS = [
     "dp_version", "dp_device_check", "dp_last_error", "dp_uniforms", "dp_sample_full",

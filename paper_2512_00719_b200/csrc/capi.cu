@@ -2,6 +2,7 @@
 // validation, launch planning and error mapping live here; kernels live in
 // sample_topk.cu / sample_general.cu / aux_kernels.cu.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "sampler.cuh"
@@ -12,6 +13,9 @@ cudaError_t launch_general(const SampleArgs& a, int dtype, int mode, int grid_ro
 size_t topk_smem_bytes(const SampleArgs& a, int mode);
 cudaError_t launch_resum(const SampleArgs& a, int dtype, cudaStream_t st);
 cudaError_t launch_warp(const SampleArgs& a, int dtype, int mode, int grid_rows, cudaStream_t st);
+int persist_grid(const SampleArgs& a, int dtype);
+size_t persist_smem_bytes(const SampleArgs& a);
+cudaError_t launch_persist(const SampleArgs& a, int dtype, int grid, cudaStream_t st);
 cudaError_t launch_row_summary(const void* logits, int dtype, int64_t B, int64_t V, int64_t ld,
                                const dp_params_t* params, const dp_penalty_t& pen, const int32_t* inv_perm,
                                double* row_max, double* total, cudaStream_t st);
@@ -153,6 +157,23 @@ bool valid_pen(const dp_penalty_t* pen, int64_t V) {
   return pen && pen->ids && pen->out_count && pen->len && pen->cap >= 0 && pen->vocab_size == V;
 }
 
+// resident CTAs of K1p for the call's shared-memory footprint (occupancy query
+// cached per (device, dtype, bytes): it runs once per shape, not per call)
+int persist_grid_cached(const dp::SampleArgs& a, int dtype) {
+  static thread_local int c_dev = -1, c_dtype = -1, c_grid = 0;
+  static thread_local size_t c_smem = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const size_t smem = dp::persist_smem_bytes(a);
+  if (dev != c_dev || dtype != c_dtype || smem != c_smem) {
+    c_grid = dp::persist_grid(a, dtype);
+    c_dev = dev;
+    c_dtype = dtype;
+    c_smem = smem;
+  }
+  return c_grid;
+}
+
 // capacities for the streaming top-k kernel (see sample_topk.cu)
 void plan_topk(dp::SampleArgs& a, const dp_plan_t* plan, int64_t B, int64_t n, int elem_bytes) {
   int32_t kmax = (plan && plan->max_top_k > 0) ? plan->max_top_k : 256;
@@ -259,8 +280,25 @@ int dp_sample_full(const void* logits, int dtype, int64_t B, int64_t V, int64_t 
   const Launches L = plan_launches(a, plan_host, dp::kFull, B, V);
   if (L.warp && (e = dp::launch_warp(a, dtype, dp::kFull, (int)B, st)) != cudaSuccess)
     return cuda_status(e, "dp_sample_full/warp");
-  if (L.topk && (e = dp::launch_topk(a, dtype, dp::kFull, (int)B, st)) != cudaSuccess)
-    return cuda_status(e, "dp_sample_full/topk");
+  if (L.topk) {
+    // several waves of rows with top-k only: the persistent warp-specialised
+    // K1p overlaps each row's final stage with the next row's stream
+    const bool no_persist = plan_host && (plan_host->flags & DP_PLAN_NO_PERSIST);
+    const int pg = (!no_persist && a.split == 1 && a.fb_rows == nullptr && !a.use_warp) ? persist_grid_cached(a, dtype)
+                                                                                         : 0;
+    if (std::getenv("DP_VERBOSE"))
+      std::fprintf(stderr, "[dp] full: B=%lld persist_grid=%d smem=%zu topk_smem=%zu kcap=%d wcap=%d lcap=%d\n",
+                   (long long)B, pg, dp::persist_smem_bytes(a), dp::topk_smem_bytes(a, dp::kFull), a.kcap, a.wcap,
+                   a.lcap);
+    // K1p pays off when the batch is one to two waves (C2: 1,024 rows on 592
+    // CTAs: the second wave's stream hides the first wave's final stages);
+    // with many waves (C4) K1's rows already interleave and its 8 streaming
+    // warps win (profiles/r2/k1p_ab.txt)
+    const bool force = plan_host && (plan_host->flags & DP_PLAN_FORCE_PERSIST);
+    if (pg > 0 && ((B > pg && B <= 2 * (int64_t)pg) || force)) e = dp::launch_persist(a, dtype, pg, st);
+    else e = dp::launch_topk(a, dtype, dp::kFull, (int)B, st);
+    if (e != cudaSuccess) return cuda_status(e, "dp_sample_full/topk");
+  }
   if (L.general && (e = dp::launch_general(a, dtype, dp::kFull, (int)B, st)) != cudaSuccess)
     return cuda_status(e, "dp_sample_full/general");
   if (nuc && (e = launch_fallback(a, dtype, dp::kFull, B, st)) != cudaSuccess)

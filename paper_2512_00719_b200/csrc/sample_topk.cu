@@ -110,6 +110,10 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
 
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u;
   const uint32_t split = (uint32_t)a.split;
+#ifdef DP_TIMELINE   // A-B build: per-row globaltimer marks into dbg.topk_ready[row * stride + 0..4]
+  auto gt = [] { uint64_t t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; };
+  uint64_t tl0 = 0, tl1 = 0, tl2 = 0;
+#endif
   const uint32_t rank = split > 1 ? cluster_ctarank() : 0u;
   const int nrows = a.row_count ? *a.row_count : a.n_rows;
   // clusters loop over rows (the tail pass launches fewer clusters than rows);
@@ -134,6 +138,9 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
   const uint32_t kp = (uint32_t)min64(n, (int64_t)ke + (MODE == kHot ? 0 : plen));
   if (route_row(a, MODE, k, plen, n) != kRouteTopk) continue;   // another kernel's row (cluster-uniform)
 
+#ifdef DP_TIMELINE
+  tl0 = gt();
+#endif
   const T* rowp = domain_row<T>(a, row, MODE);
   const int32_t* pids = a.pen.ids + (int64_t)row * a.pen.cap;
   const int32_t* pcnt = a.pen.out_count + (int64_t)row * a.pen.cap;
@@ -474,6 +481,9 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
   }
 
   lapk(18);
+#ifdef DP_TIMELINE
+  tl1 = gt();
+#endif
   if (tid == 0) touch_bytes(a, row, loaded);
   // ---- CTA-level exact top-kp
   {
@@ -549,12 +559,24 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
   }
 
   lapk(20);
+#ifdef DP_TIMELINE
+  tl2 = gt();
+#endif
   // ---- final stage (CTA 0): penalties, exact sort, filter, draw
   {
     const FinLayout F = fin_layout(a.lcap);
     finish_row<T, MODE, NT, NUC>(a, row, p, plen, rowp, lo, n, sel, ms.nsel, sh_cta, mrow, smem + L.cand, F, ms.fin,
                                  tid, [] { __syncthreads(); }, nullptr, mtau_hi);
   }
+#ifdef DP_TIMELINE
+  __syncthreads();
+  if (tid == 0 && a.dbg.topk_ready) {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    double* tl = a.dbg.topk_ready + (int64_t)row * a.dbg.topk_stride;
+    tl[0] = (double)tl0; tl[1] = (double)tl1; tl[2] = (double)tl2; tl[3] = (double)gt(); tl[4] = (double)smid;
+  }
+#endif
   if (split > 1) {
     if (ridx + (int)(gridDim.x / split) >= nrows) {   // last row: the cluster's final barrier, then exit
 #ifndef DP_CLUSTER_EARLY_RETIRE

@@ -323,24 +323,44 @@ DP_DEV DrawResult warp_filter_draw_smem(const double* r, int32_t k, const dp_par
 }
 
 // k <= 64: everything in registers (two candidates per lane)
+#ifdef DP_DRAW_PROBE
+__device__ long long g_probe[32];
+__device__ int g_probe_base;
+#define PROBE(i) do { long long _n = clock64(); if (lane == 0) atomicAdd((unsigned long long*)&g_probe[g_probe_base + (i)], (unsigned long long)(_n - _pc)); _pc = _n; } while (0)
+#else
+#define PROBE(i) do { } while (0)
+#endif
 DP_DEV DrawResult warp_filter_draw_reg(const double* r, int32_t k, const dp_params_t& p, double u) {
   // compact on purpose: this runs once per row with a cold instruction cache,
   // so every instruction it does not have is ~20 cycles saved
   const uint32_t lane = lane_id();
+#ifdef DP_DRAW_SYNCWARP
+  __syncwarp();
+#endif
+#ifdef DP_DRAW_PROBE
+  long long _pc = clock64();
+#endif
   const int32_t j0 = lane, j1 = lane + 32;
   const double r0 = __shfl_sync(0xffffffffu, r[0], 0);
-  double rr[2], ww[2];
+  // both candidates of a lane through ONE exp call on a lane-local pair: a
+  // loop over an array (rr[h]) would put the pair in local memory, whose
+  // store -> load round trip costs more than the whole draw
+  const double ra = j0 < k ? r[j0] : 0.0;
+  const double rb = j1 < k ? r[j1] : 0.0;
+  double wa = 0.0, wb = 0.0;
 #pragma unroll 1
   for (int h = 0; h < 2; ++h) {   // one copy of the f64 exp
-    const int32_t j = (int32_t)lane + 32 * h;
-    rr[h] = j < k ? r[j] : 0.0;
-    ww[h] = j < k ? exp(rr[h] - r0) : 0.0;
+    const bool in = (h == 0 ? j0 : j1) < k;
+    const double e = in ? exp((h == 0 ? ra : rb) - r0) : 0.0;
+    if (h == 0) wa = e;
+    else wb = e;
   }
-  const double ra = rr[0], rb = rr[1], wa = ww[0], wb = ww[1];
+  PROBE(0);
   const double ca = warp_incl_scan(wa);
   const double tot_a = __shfl_sync(0xffffffffu, ca, 31);
   const double cb = warp_incl_scan(wb) + tot_a;
   const double total = __shfl_sync(0xffffffffu, cb, 31);
+  PROBE(1);
   // value at global index j (any lane): cum / w / r via shuffles
   auto cum_at = [&](int32_t j) -> double { return __shfl_sync(0xffffffffu, j < 32 ? ca : cb, j & 31); };
   auto w_at = [&](int32_t j) -> double { return __shfl_sync(0xffffffffu, j < 32 ? wa : wb, j & 31); };
@@ -359,6 +379,7 @@ DP_DEV DrawResult warp_filter_draw_reg(const double* r, int32_t k, const dp_para
     for (int32_t j = max(0, kp - 2); j < min(k, kp + 1); ++j) margin = fmin(margin, fabs(cum_at(j) - thr));
     margin = ratio(margin, total);
   }
+  PROBE(2);
   if (p.min_p > 0.0) {
     const double floor_ = p.min_p * 1.0;   // w_0 = exp(0) = 1
     const int32_t ge = __popc(__ballot_sync(0xffffffffu, j0 < k && wa >= floor_)) +
@@ -368,6 +389,7 @@ DP_DEV DrawResult warp_filter_draw_reg(const double* r, int32_t k, const dp_para
     for (int32_t j = max(0, ge - 1); j < min(k, ge + 1); ++j) margin = fmin(margin, fabs(w_at(j) - floor_));
   }
   kept = max(1, kept);
+  PROBE(3);
   const double S = cum_at(kept - 1);
   const double us = u * S;
   const int32_t le = __popc(__ballot_sync(0xffffffffu, j0 < kept && ca <= us)) +
@@ -381,6 +403,7 @@ DP_DEV DrawResult warp_filter_draw_reg(const double* r, int32_t k, const dp_para
   // ln p_j = ln(w_j / S) = (r_j - r_0) - ln S (w_j = exp(r_j - r_0))
   res.logprob = (r_at(js) - r0) - log(S);
   res.margin = fmin(margin, ratio(dm, S));
+  PROBE(4);
   return res;
 }
 
@@ -457,7 +480,15 @@ DP_DEV DrawResult warp_filter_draw_nuc(const double* r, int32_t K, const dp_para
   return res;
 }
 
-DP_DEV DrawResult warp_filter_draw(const double* r, int32_t k, const dp_params_t& p, double u, double* w,
+// A real call, not inlined: inlined into finish_row's large body the draw
+// compiled to ~15k cycles per row (measured, tools/micro/finish.cu); as its
+// own function it runs in ~2.6k (call overhead included)
+#ifndef DP_DRAW_INLINE
+static __device__ __noinline__
+#else
+DP_DEV
+#endif
+DrawResult warp_filter_draw(const double* r, int32_t k, const dp_params_t& p, double u, double* w,
                                    double* cum, int64_t* prof = nullptr) {
   (void)prof;
   return k <= 64 ? warp_filter_draw_reg(r, k, p, u) : warp_filter_draw_smem(r, k, p, u, w, cum);

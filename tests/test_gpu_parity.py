@@ -925,3 +925,44 @@ def test_dropin_sample_full_and_shvs_sample(torch_cuda):
         d = shvs_sample(ShvsRowContext(row, m, s_tot), hot, SamplingParams(**vars(p)), u, 3, 0)
         want = O.sample_shvs_row(row, O.State.new([], 8192), p, u, hot_ids, tail)
         assert (d.token_id == want.token and d.accepted_hot == want.accepted_hot) or want.margin < EPS
+
+
+@pytest.mark.parametrize("bf16", [False, True])
+def test_persistent_k1_equals_per_row_k1(torch_cuda, bf16):
+    """K1p (persistent, warp-specialised; dp_sample_full picks it when the
+    batch spans one to two waves, forced here) and K1 (one CTA per row, DP_PLAN_NO_PERSIST)
+    make bit-identical decisions and penalty updates over 4 iterations of the
+    C2 workload with a heterogeneous top-k mix (k = 1 .. 200), and both match
+    the oracle on sampled rows."""
+    torch = torch_cuda
+    from paper_2512_00719_b200 import _native as N
+    from paper_2512_00719_b200.synthetic import SyntheticSource
+
+    v, bsz = 152064, 1536
+    ks = [1, 7, 50, 200]
+    params = [O.Params(**dict(_bench_params(False, b).__dict__, top_k=ks[b % 4], seed=b)) for b in range(bsz)]
+    prompts = [np.random.default_rng(b).integers(0, v, 8 + b % 64) for b in range(bsz)]
+    a = plane_for(torch, v, params, prompts)
+    a._plan.flags = N.PLAN_FORCE_PERSIST
+    b_ = plane_for(torch, v, params, prompts)
+    b_._plan.flags = N.PLAN_NO_PERSIST
+    src = SyntheticSource(v, device="cuda")
+    check = list(range(0, bsz, 97))
+    states = {b: O.State.new(prompts[b], v) for b in check}
+    exempt = []
+    dt = torch.bfloat16 if bf16 else torch.float32
+    for it in range(4):
+        x = src.generate(it, range(bsz), dtype=dt)
+        da = a.sample(x, it)
+        ta, la, fa = da.token.clone(), da.logprob.clone(), da.flags.clone()
+        db = b_.sample(x, it)
+        assert torch.equal(ta, db.token) and torch.equal(la, db.logprob) and torch.equal(fa, db.flags)
+        xh = x[check].float().cpu().numpy()
+        dec = [O.sample_full_row(xh[i], states[b], params[b], O.uniforms_per_row([params[b].seed], it, [b])[0])
+               for i, b in enumerate(check)]
+        compare(f"persist/it{it}", ta.cpu().numpy()[check], la.cpu().numpy()[check], dec, exempt, lp_tol=1e-6)
+        for b in check:
+            states[b].update(int(ta[b]))
+    ra, rb = a.state.rows(), b_.state.rows()
+    for b in range(0, bsz, 13):
+        assert np.array_equal(ra[b][0], rb[b][0]) and np.array_equal(ra[b][1], rb[b][1])

@@ -2,6 +2,7 @@
 // kernel) in a 256-thread CTA, with the top-k kernel's launch bounds.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I include tools/micro/finish.cu -o tools/micro/finish
 #include <cstdio>
+#include <cstdlib>
 #include <vector>
 #include "../../paper_2512_00719_b200/csrc/finish.cuh"
 using namespace dp;
@@ -18,14 +19,52 @@ __global__ void __launch_bounds__(256, MB) kern(SampleArgs a, const float* row, 
   for (int i = t; i < nsel_in; i += 256) sel[i] = comp_key(row[i], (uint32_t)i);
   const dp_params_t p = a.params[0];
   __syncthreads();
+  {   // the draw with a COLD instruction cache: first code this kernel runs after setup
+    const double* frc = reinterpret_cast<const double*>(smem + F.r);
+    for (int i = t; i < 64; i += 256) reinterpret_cast<double*>(smem + F.r)[i] = -0.05 * i;
+    __syncthreads();
+    if (t < 32) {
+      long long c0 = clock64();
+      DrawResult d = warp_filter_draw(frc, 50, p, 0.37, reinterpret_cast<double*>(smem + F.w),
+                                      reinterpret_cast<double*>(smem + F.cum), nullptr);
+      long long c1 = clock64();
+      if (t == 0) { cyc[6] = c1 - c0; if (d.index == -3) cyc[7] = 2; }
+    }
+    __syncthreads();
+  }
+#ifdef DP_DRAW_PROBE
+  if (t == 0) g_probe_base = 0;
+#endif
+  __syncthreads();
   long long t0 = clock64();
+  long long inter = 0;
   for (int it = 0; it < 4; ++it) {
     finish_row<float, kTail, 256, false>(a, 0, p, plen, row, 0, n, sel, nsel_in, 0.0, 0.0, smem, F, fs, t,
                                   [] { __syncthreads(); });
     __syncthreads();
+    // the same draw right after finish_row, interleaved (i-cache probe)
+    if (t < 32) {
+      const double* fr0 = reinterpret_cast<const double*>(smem + F.r);
+#ifdef DP_DRAW_PROBE
+      if (t == 0) g_probe_base = 8;  // standalone copy
+#endif
+      __syncwarp();
+      long long q0 = clock64();
+      if (t == 0) atomicAdd((unsigned long long*)&a.dbg.stats[20], 1ull);   // like lap(14) right before the draw
+      DrawResult d = warp_filter_draw(fr0, p.top_k, p, 0.41, reinterpret_cast<double*>(smem + F.w),
+                                      reinterpret_cast<double*>(smem + F.cum), nullptr);
+      long long q1 = clock64();
+      inter += q1 - q0;
+      if (d.index == -5) cyc[7] = 1;
+#ifdef DP_DRAW_PROBE
+      if (t == 0) g_probe_base = 0;
+#endif
+      __syncwarp();
+    }
+    __syncthreads();
   }
   long long t1 = clock64();
-  if (t == 0) cyc[0] = (t1 - t0) / 4;
+  if (t == 0) { cyc[0] = (t1 - t0) / 4; cyc[5] = inter / 4; }
   // the draw alone, on the final list finish_row left in shared memory
   double* fr = reinterpret_cast<double*>(smem + F.r);
   double* fw = reinterpret_cast<double*>(smem + F.w);
@@ -47,7 +86,8 @@ __global__ void __launch_bounds__(256, MB) kern(SampleArgs a, const float* row, 
   }
 }
 
-int main() {
+int main(int argc, char** argv) {
+  const int nblk = argc > 1 ? atoi(argv[1]) : 1;
   const int n = 8192, plen = 100, cap = 256, nsel = 150;
   std::vector<float> h(n);
   for (int i = 0; i < n; ++i) h[i] = (i < 1000) ? 5.0f - 0.004f * i : -3.0f - 1e-4f * i;
@@ -75,16 +115,23 @@ int main() {
   const FinLayout F = fin_layout(a.lcap);
   for (int mb : {1, 2, 4}) {
     for (int rep = 0; rep < 2; ++rep) {
-      if (mb == 1) { cudaFuncSetAttribute(kern<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, F.bytes); kern<1><<<1, 256, F.bytes>>>(a, row, n, plen, nsel, cyc); }
-      if (mb == 2) { cudaFuncSetAttribute(kern<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, F.bytes); kern<2><<<1, 256, F.bytes>>>(a, row, n, plen, nsel, cyc); }
-      if (mb == 4) { cudaFuncSetAttribute(kern<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, F.bytes); kern<4><<<1, 256, F.bytes>>>(a, row, n, plen, nsel, cyc); }
+      if (mb == 1) { cudaFuncSetAttribute(kern<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, F.bytes); kern<1><<<nblk, 256, F.bytes>>>(a, row, n, plen, nsel, cyc); }
+      if (mb == 2) { cudaFuncSetAttribute(kern<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, F.bytes); kern<2><<<nblk, 256, F.bytes>>>(a, row, n, plen, nsel, cyc); }
+      if (mb == 4) { cudaFuncSetAttribute(kern<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, F.bytes); kern<4><<<nblk, 256, F.bytes>>>(a, row, n, plen, nsel, cyc); }
       cudaError_t e = cudaDeviceSynchronize();
       if (e != cudaSuccess) { printf("err %s\n", cudaGetErrorString(e)); return 1; }
     }
     int tk; cudaMemcpy(&tk, tok, 4, cudaMemcpyDeviceToHost);
-    printf("  laps/row: 12 %lld 13 %lld 14 %lld 16 %lld 15 %lld\n", st[12] / 8, st[13] / 8, st[14] / 8, st[16] / 8, st[15] / 8);
+    printf("  laps/row: 12 %lld 13 %lld 14 %lld 16 %lld 15 %lld 21(2nd draw) %lld\n", st[12] / (8 * nblk), st[13] / (8 * nblk), st[14] / (8 * nblk), st[16] / (8 * nblk), st[15] / (8 * nblk), st[21] / (8 * nblk));
     for (int i = 0; i < 24; ++i) st[i] = 0;
-    printf("finish_row minBlocks=%d: %lld cycles (token %d); draw in loop %lld, draw once %lld\n", mb, cyc[0], tk, cyc[1], cyc[2]);
+    printf("[%d CTAs] finish_row minBlocks=%d: %lld cycles (token %d); draw in loop %lld, draw once %lld, draw interleaved with finish_row %lld, draw COLD %lld\n", nblk, mb, cyc[0], tk, cyc[1], cyc[2], cyc[5], cyc[6]);
   }
+#ifdef DP_DRAW_PROBE
+  long long hprobe[32];
+  cudaMemcpyFromSymbol(hprobe, g_probe, sizeof(hprobe));
+  printf("probe (finish_row ctx, cumulative): %lld %lld %lld %lld %lld\n", hprobe[0], hprobe[1], hprobe[2], hprobe[3], hprobe[4]);
+  printf("probe (standalone ctx, cumulative): %lld %lld %lld %lld %lld\n", hprobe[8], hprobe[9], hprobe[10], hprobe[11], hprobe[12]);
+  printf("probe (finish_row ctx, 2nd run):    %lld %lld %lld %lld %lld\n", hprobe[16], hprobe[17], hprobe[18], hprobe[19], hprobe[20]);
+#endif
   return 0;
 }

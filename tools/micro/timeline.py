@@ -1,0 +1,46 @@
+"""Per-row timeline of the K1 kernel (DP_TIMELINE build via DP_LIB):
+row start, end of stream, end of select/merge, end of finish, SM id.
+    DP_LIB=.../timeline.so python tools/micro/timeline.py [--config c2]"""
+import argparse, os, sys, json
+import numpy as np
+import torch
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+import bench
+from paper_2512_00719_b200 import DecisionPlane
+from paper_2512_00719_b200.synthetic import SyntheticSource
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="c2")
+ap.add_argument("--out", default=None)
+args = ap.parse_args()
+cfg = bench.CONFIGS[args.config]
+v, b = cfg["V"], cfg["B"]
+prompts = [np.random.default_rng(s).integers(0, v, 32) for s in range(b)]
+src = SyntheticSource(v, device="cuda")
+plane = DecisionPlane(v, [bench.row_params(cfg, s) for s in range(b)], prompts=prompts, max_generated=136)
+dt = torch.bfloat16 if cfg["dtype"] == "bf16" else torch.float32
+xs = [src.generate(i, range(b), dtype=dt) for i in range(2)]
+for i in range(4):
+    d = plane.sample(xs[i & 1], i, debug=True, topk_stride=8, update=False)
+torch.cuda.synchronize()
+tl = d.topk_ready.cpu().numpy()[:, :5]
+t0 = tl[:, 0].min()
+r = (tl[:, :4] - t0) / 1e3
+sm = tl[:, 4].astype(int)
+stream = r[:, 1] - r[:, 0]; sel = r[:, 2] - r[:, 1]; fin = r[:, 3] - r[:, 2]
+print(f"span {r[:, 3].max():.1f} us; per row: stream {np.median(stream):.1f} (p10 {np.percentile(stream,10):.1f} p90 {np.percentile(stream,90):.1f}) "
+      f"select {np.median(sel):.1f} finish {np.median(fin):.1f} us")
+order = np.argsort(r[:, 0])
+starts = np.sort(r[:, 0])
+print("row starts (us) deciles:", np.round(np.percentile(starts, np.arange(0, 101, 10)), 1).tolist())
+print("row ends (us) deciles:", np.round(np.percentile(r[:, 3], np.arange(0, 101, 10)), 1).tolist())
+# how many rows are streaming / finishing at each microsecond
+grid = np.arange(0, r[:, 3].max() + 1, 2.0)
+streaming = [(np.sum((r[:, 0] <= t) & (r[:, 1] > t))) for t in grid]
+finishing = [(np.sum((r[:, 1] <= t) & (r[:, 3] > t))) for t in grid]
+print("t(us) streaming finishing:")
+for t, s_, f_ in zip(grid, streaming, finishing):
+    print(f"  {t:6.1f} {s_:4d} {f_:4d}")
+if args.out:
+    np.save(args.out, tl)
