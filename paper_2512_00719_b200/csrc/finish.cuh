@@ -557,22 +557,9 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
       const double ref = MODE == kHot ? mrow : cref_r;
       const double total = s_dom * exp(ref - fr[0]);
       if (!(total > 0.0) || !isfinite(total)) fb = true;   // e.g. the first batch missed the row's scale
-      else d = warp_filter_draw_nuc(fr, (int32_t)min((uint32_t)k, nl), p, ud, total, fw, fcum, fb);
+      else d = warp_filter_draw_nuc(fr, (int32_t)min((uint32_t)k, nl), knobs_of(p), ud, total, fw, fcum, fb);
     } else {
-#ifdef DP_DRAW_TWICE   // A-B probe: the SAME code twice (the second run is warm), cycles into stats[21]
-#pragma unroll 1
-      for (int rep = 0; rep < 2; ++rep) {
-#ifdef DP_DRAW_PROBE
-        if (lane == 0) g_probe_base = rep * 16;
-        __syncwarp();
-#endif
-        d = warp_filter_draw(fr, (int32_t)min((uint32_t)k, nl), p, ud, fw, fcum, a.dbg.stats);
-        if (rep == 0) lap(16);
-      }
-      lap(21);
-#else
-      d = warp_filter_draw(fr, (int32_t)min((uint32_t)k, nl), p, ud, fw, fcum, a.dbg.stats);
-#endif
+      d = warp_filter_draw(fr, (int32_t)min((uint32_t)k, nl), knobs_of(p), ud, fw, fcum, a.dbg.stats);
     }
     lap(16);
 

@@ -574,7 +574,7 @@ __global__ void __launch_bounds__(kMW * 32, kMWBlocks) warp_sample_kernel(Sample
       }
       continue;
     }
-    const DrawResult d = warp_filter_draw_reg(F.fr, (int32_t)kk, p, u[0]);
+    const DrawResult d = warp_filter_draw_reg(F.fr, (int32_t)kk, knobs_of(p), u[0]);
     lap(7);
     if (prof) atomicMax((unsigned long long*)&a.dbg.stats[22], gtime());
     if (lane == 0) {

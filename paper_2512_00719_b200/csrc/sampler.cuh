@@ -72,7 +72,6 @@ DP_DEV const T* domain_row(const SampleArgs& a, int row, int mode) {
   if (mode == kTail && a.tail_logits) return reinterpret_cast<const T*>(a.tail_logits) + (int64_t)row * a.tail_ld;
   return reinterpret_cast<const T*>(a.logits) + (int64_t)row * a.ld + dom_lo(a, mode);
 }
-// raw logit at an absolute row position (either storage)
 // VisitCounter (instrument.py:6-33) on the device: bytes this launch loaded
 // for `row` — every streaming pass (re-streams included), scalar head / tail
 // elements and gathered penalty values — accumulated per row across the
@@ -82,6 +81,7 @@ DP_DEV void touch_bytes(const SampleArgs& a, int row, uint64_t bytes) {
     atomicAdd(reinterpret_cast<unsigned long long*>(a.dbg.bytes_touched + row), (unsigned long long)bytes);
 }
 
+// raw logit at an absolute row position (either storage)
 template <typename T>
 DP_DEV float row_value(const SampleArgs& a, int row, int64_t pos) {
   if (a.tail_logits && pos >= a.H)
@@ -253,6 +253,14 @@ DP_DEV void push_resum(const SampleArgs& a, int row, double sH) {
 // Executed by ONE warp.  r[0..n) ready values (f64, sorted), n >= 1;
 // `k` = number of candidates entering the top-p / min-p stages (the top-k
 // set, or the whole domain when top-k is off).  w / cum are scratch [n].
+// the filter knobs a draw needs, passed by value: a `const dp_params_t&`
+// argument of a non-inlined draw would force the caller's params into local
+// memory
+struct DrawKnobs {
+  double top_p, min_p;
+};
+DP_DEV DrawKnobs knobs_of(const dp_params_t& p) { return DrawKnobs{p.top_p, p.min_p}; }
+
 struct DrawResult {
   int32_t index;     // position in the sorted list
   int32_t kept;
@@ -260,7 +268,7 @@ struct DrawResult {
   double margin;
 };
 
-DP_DEV DrawResult warp_filter_draw_smem(const double* r, int32_t k, const dp_params_t& p, double u, double* w,
+DP_DEV DrawResult warp_filter_draw_smem(const double* r, int32_t k, const DrawKnobs p, double u, double* w,
                                         double* cum) {
   const uint32_t lane = lane_id();
   const double r0 = r[0];
@@ -323,23 +331,10 @@ DP_DEV DrawResult warp_filter_draw_smem(const double* r, int32_t k, const dp_par
 }
 
 // k <= 64: everything in registers (two candidates per lane)
-#ifdef DP_DRAW_PROBE
-__device__ long long g_probe[32];
-__device__ int g_probe_base;
-#define PROBE(i) do { long long _n = clock64(); if (lane == 0) atomicAdd((unsigned long long*)&g_probe[g_probe_base + (i)], (unsigned long long)(_n - _pc)); _pc = _n; } while (0)
-#else
-#define PROBE(i) do { } while (0)
-#endif
-DP_DEV DrawResult warp_filter_draw_reg(const double* r, int32_t k, const dp_params_t& p, double u) {
+DP_DEV DrawResult warp_filter_draw_reg(const double* r, int32_t k, const DrawKnobs p, double u) {
   // compact on purpose: this runs once per row with a cold instruction cache,
   // so every instruction it does not have is ~20 cycles saved
   const uint32_t lane = lane_id();
-#ifdef DP_DRAW_SYNCWARP
-  __syncwarp();
-#endif
-#ifdef DP_DRAW_PROBE
-  long long _pc = clock64();
-#endif
   const int32_t j0 = lane, j1 = lane + 32;
   const double r0 = __shfl_sync(0xffffffffu, r[0], 0);
   // both candidates of a lane through ONE exp call on a lane-local pair: a
@@ -355,12 +350,10 @@ DP_DEV DrawResult warp_filter_draw_reg(const double* r, int32_t k, const dp_para
     if (h == 0) wa = e;
     else wb = e;
   }
-  PROBE(0);
   const double ca = warp_incl_scan(wa);
   const double tot_a = __shfl_sync(0xffffffffu, ca, 31);
   const double cb = warp_incl_scan(wb) + tot_a;
   const double total = __shfl_sync(0xffffffffu, cb, 31);
-  PROBE(1);
   // value at global index j (any lane): cum / w / r via shuffles
   auto cum_at = [&](int32_t j) -> double { return __shfl_sync(0xffffffffu, j < 32 ? ca : cb, j & 31); };
   auto w_at = [&](int32_t j) -> double { return __shfl_sync(0xffffffffu, j < 32 ? wa : wb, j & 31); };
@@ -379,7 +372,6 @@ DP_DEV DrawResult warp_filter_draw_reg(const double* r, int32_t k, const dp_para
     for (int32_t j = max(0, kp - 2); j < min(k, kp + 1); ++j) margin = fmin(margin, fabs(cum_at(j) - thr));
     margin = ratio(margin, total);
   }
-  PROBE(2);
   if (p.min_p > 0.0) {
     const double floor_ = p.min_p * 1.0;   // w_0 = exp(0) = 1
     const int32_t ge = __popc(__ballot_sync(0xffffffffu, j0 < k && wa >= floor_)) +
@@ -389,7 +381,6 @@ DP_DEV DrawResult warp_filter_draw_reg(const double* r, int32_t k, const dp_para
     for (int32_t j = max(0, ge - 1); j < min(k, ge + 1); ++j) margin = fmin(margin, fabs(w_at(j) - floor_));
   }
   kept = max(1, kept);
-  PROBE(3);
   const double S = cum_at(kept - 1);
   const double us = u * S;
   const int32_t le = __popc(__ballot_sync(0xffffffffu, j0 < kept && ca <= us)) +
@@ -403,7 +394,6 @@ DP_DEV DrawResult warp_filter_draw_reg(const double* r, int32_t k, const dp_para
   // ln p_j = ln(w_j / S) = (r_j - r_0) - ln S (w_j = exp(r_j - r_0))
   res.logprob = (r_at(js) - r0) - log(S);
   res.margin = fmin(margin, ratio(dm, S));
-  PROBE(4);
   return res;
 }
 
@@ -412,7 +402,7 @@ DP_DEV DrawResult warp_filter_draw_reg(const double* r, int32_t k, const dp_para
 // Same law as warp_filter_draw over the full domain (filtering.py:61-162);
 // exact whenever the kept set — and for neutral rows the draw — lies inside
 // the list.  `fallback` is set otherwise (the general kernel decides).
-DP_DEV DrawResult warp_filter_draw_nuc(const double* r, int32_t K, const dp_params_t& p, double u, double total,
+DP_DEV DrawResult warp_filter_draw_nuc(const double* r, int32_t K, const DrawKnobs p, double u, double total,
                                        double* w, double* cum, bool& fallback) {
   const uint32_t lane = lane_id();
   const double r0 = r[0];
@@ -480,15 +470,14 @@ DP_DEV DrawResult warp_filter_draw_nuc(const double* r, int32_t K, const dp_para
   return res;
 }
 
-// A real call, not inlined: inlined into finish_row's large body the draw
-// compiled to ~15k cycles per row (measured, tools/micro/finish.cu); as its
-// own function it runs in ~2.6k (call overhead included)
+// A real call, not inlined: one compiled copy shared by every final stage
+// (smaller code), ~2.4k cycles on an idle SM (tools/micro/finish.cu)
 #ifndef DP_DRAW_INLINE
 static __device__ __noinline__
 #else
 DP_DEV
 #endif
-DrawResult warp_filter_draw(const double* r, int32_t k, const dp_params_t& p, double u, double* w,
+DrawResult warp_filter_draw(const double* r, int32_t k, const DrawKnobs p, double u, double* w,
                                    double* cum, int64_t* prof = nullptr) {
   (void)prof;
   return k <= 64 ? warp_filter_draw_reg(r, k, p, u) : warp_filter_draw_smem(r, k, p, u, w, cum);

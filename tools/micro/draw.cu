@@ -12,7 +12,7 @@ __global__ void kern(double* out, long long* cyc, int k, int iters) {
   double acc = 0;
   long long t0 = clock64();
   for (int it = 0; it < iters; ++it) {
-    DrawResult d = warp_filter_draw(r, k, p, 0.3 + 1e-4 * it, w, cum);
+    DrawResult d = warp_filter_draw(r, k, knobs_of(p), 0.3 + 1e-4 * it, w, cum);
     acc += d.logprob + d.index;
   }
   long long t1 = clock64();

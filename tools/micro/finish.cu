@@ -25,7 +25,7 @@ __global__ void __launch_bounds__(256, MB) kern(SampleArgs a, const float* row, 
     __syncthreads();
     if (t < 32) {
       long long c0 = clock64();
-      DrawResult d = warp_filter_draw(frc, 50, p, 0.37, reinterpret_cast<double*>(smem + F.w),
+      DrawResult d = warp_filter_draw(frc, 50, knobs_of(p), 0.37, reinterpret_cast<double*>(smem + F.w),
                                       reinterpret_cast<double*>(smem + F.cum), nullptr);
       long long c1 = clock64();
       if (t == 0) { cyc[6] = c1 - c0; if (d.index == -3) cyc[7] = 2; }
@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(256, MB) kern(SampleArgs a, const float* row, 
       __syncwarp();
       long long q0 = clock64();
       if (t == 0) atomicAdd((unsigned long long*)&a.dbg.stats[20], 1ull);   // like lap(14) right before the draw
-      DrawResult d = warp_filter_draw(fr0, p.top_k, p, 0.41, reinterpret_cast<double*>(smem + F.w),
+      DrawResult d = warp_filter_draw(fr0, p.top_k, knobs_of(p), 0.41, reinterpret_cast<double*>(smem + F.w),
                                       reinterpret_cast<double*>(smem + F.cum), nullptr);
       long long q1 = clock64();
       inter += q1 - q0;
@@ -74,13 +74,13 @@ __global__ void __launch_bounds__(256, MB) kern(SampleArgs a, const float* row, 
     double acc = 0;
     long long d0 = clock64();
     for (int it = 0; it < 10; ++it) {
-      DrawResult d = warp_filter_draw(fr, p.top_k, p, 0.3 + 1e-3 * it, fw, fc, a.dbg.stats);
+      DrawResult d = warp_filter_draw(fr, p.top_k, knobs_of(p), 0.3 + 1e-3 * it, fw, fc, a.dbg.stats);
       acc += d.logprob;
     }
     long long d1 = clock64();
     if (t == 0) { cyc[1] = (d1 - d0) / 10; cyc[3] = (long long)acc; }
     d0 = clock64();
-    DrawResult d = warp_filter_draw(fr, p.top_k, p, 0.77, fw, fc, a.dbg.stats);
+    DrawResult d = warp_filter_draw(fr, p.top_k, knobs_of(p), 0.77, fw, fc, a.dbg.stats);
     d1 = clock64();
     if (t == 0) { cyc[2] = d1 - d0; cyc[4] = d.index; }
   }
