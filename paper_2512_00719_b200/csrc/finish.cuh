@@ -74,29 +74,40 @@ DP_DEV PenPrefetch pen_prefetch(const SampleArgs& a, int row, int32_t plen, cons
 // Descending bitonic sort of 32*E (u64 key, u32 pos) pairs held in registers
 // by one warp; element i = j*32 + lane lives in slot j of lane `lane`.
 // Order: key desc, pos asc (the canonical (value desc, id asc) rule).
+// The (size, stride) stages are a rolled loop: the sort runs once per row with
+// a cold instruction cache, and the fully unrolled network (thousands of
+// instructions for E = 8) was fetched from L2 line by line every row
+// (no_instructions stalls, profiles/r2); only the slot loop is unrolled so the
+// register arrays stay in registers.
+template <int E, int JS>
+DP_DEV void warp_reg_sort_cross(uint64_t (&key)[E], uint32_t (&pos)[E], uint32_t lane, int size) {
+#pragma unroll
+  for (int j = 0; j < E; ++j) {
+    if ((j & JS) == 0) {
+      const int jp = j | JS;
+      const uint32_t i = (uint32_t)j * 32u + lane;
+      const bool desc = (i & (uint32_t)size) == 0u;
+      const bool a_first = key[j] > key[jp] || (key[j] == key[jp] && pos[j] < pos[jp]);
+      if (a_first != desc) {
+        const uint64_t tk = key[j]; key[j] = key[jp]; key[jp] = tk;
+        const uint32_t tp = pos[j]; pos[j] = pos[jp]; pos[jp] = tp;
+      }
+    }
+  }
+}
 template <int E>
 DP_DEV void warp_reg_sort(uint64_t (&key)[E], uint32_t (&pos)[E]) {
   const uint32_t lane = lane_id();
   constexpr int N = 32 * E;
-#pragma unroll
+#pragma unroll 1
   for (int size = 2; size <= N; size <<= 1) {
-#pragma unroll
+#pragma unroll 1
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
       if (stride >= 32) {
         const int js = stride / 32;
-#pragma unroll
-        for (int j = 0; j < E; ++j) {
-          if ((j & js) == 0) {
-            const int jp = j | js;
-            const uint32_t i = (uint32_t)j * 32u + lane;
-            const bool desc = (i & (uint32_t)size) == 0u;
-            const bool a_first = key[j] > key[jp] || (key[j] == key[jp] && pos[j] < pos[jp]);
-            if (a_first != desc) {
-              const uint64_t tk = key[j]; key[j] = key[jp]; key[jp] = tk;
-              const uint32_t tp = pos[j]; pos[j] = pos[jp]; pos[jp] = tp;
-            }
-          }
-        }
+        if constexpr (E >= 2) { if (js == 1) warp_reg_sort_cross<E, 1>(key, pos, lane, size); }
+        if constexpr (E >= 4) { if (js == 2) warp_reg_sort_cross<E, 2>(key, pos, lane, size); }
+        if constexpr (E >= 8) { if (js == 4) warp_reg_sort_cross<E, 4>(key, pos, lane, size); }
       } else {
         const bool lower = (lane & (uint32_t)stride) == 0u;
 #pragma unroll

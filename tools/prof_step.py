@@ -28,6 +28,8 @@ def main():
     ap.add_argument("--kernel", type=int, default=0)
     ap.add_argument("--hot", type=int, default=4096)
     ap.add_argument("--bf16", action="store_true")
+    ap.add_argument("--extra", default="", help="comma list: fused (producer-fused summary), curve (K6), "
+                                                "summary (K2 penalized)")
     args = ap.parse_args()
     cfg = bench.CONFIGS[args.config]
     v, b = cfg["V"], cfg["B"]
@@ -39,8 +41,16 @@ def main():
                           max_generated=136)
     perm = hot.device_maps(plane.device)[0] if hot is not None else None
     dt = torch.bfloat16 if (args.bf16 or cfg["dtype"] == "bf16") else torch.float32
-    x = src.generate(0, range(b), dtype=dt, perm=perm)
-    summ = plane.producer_summary(x) if args.variant == "shvs" else None
+    extra = set(filter(None, args.extra.split(",")))
+    if "fused" in extra:
+        x, summ = src.generate(0, range(b), dtype=dt, perm=perm, summary_params=plane.params_dev)
+    else:
+        x = src.generate(0, range(b), dtype=dt, perm=perm)
+        summ = plane.producer_summary(x) if args.variant == "shvs" else None
+    if "curve" in extra and hot is not None:
+        plane.hot_mass_curve(x, [256, 512, 1024, 2048, 4096, 8192, 16384, 32768])
+    if "summary" in extra:
+        plane.row_summary(x, inv_perm=hot.device_maps(plane.device)[1] if hot is not None else None)
     for i in range(args.steps):
         if args.variant == "shvs":
             plane.sample(x, i, variant="shvs", summary=summ, summary_raw=True)
