@@ -548,7 +548,7 @@ def run_ours(args, cfg):
     prompts = [np.random.default_rng(int(s)).integers(0, v, PROMPT_LEN) for s in seq_ids]
     params = [row_params(cfg, int(s)) for s in seq_ids]
     src = SyntheticSource(v, device=dev)
-    variant = args.variant if not cfg.get("mix") else "shvs"
+    variant = args.variant or ("shvs" if cfg.get("mix") else "full")
     hot = None
     plane = DecisionPlane(v, params, prompts=prompts, seq_ids=seq_ids, hot=hot, device=dev,
                           max_generated=RESET_EVERY + 8, split=args.split, kernel=args.kernel)
@@ -773,7 +773,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=None, choices=sorted(CONFIGS),
                     help="default: c2 on one GPU, c4 (B=8,192 split over the ranks, strong scaling) on N > 1")
-    ap.add_argument("--variant", default="full", choices=["full", "shvs"])
+    ap.add_argument("--variant", default=None, choices=["full", "shvs"],
+                    help="default: full (C5: shvs, the config's SHVS mix)")
     ap.add_argument("--split", type=int, default=0)
     ap.add_argument("--kernel", type=int, default=0, help="dp_plan_t.kernel: 0 auto, 1 CTA/cluster, 2 warp-per-row")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)

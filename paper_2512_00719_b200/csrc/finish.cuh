@@ -370,7 +370,13 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
   const double cref_r = (double)cref / p.temperature;   // cref in ready units
   // the rank-merge path keeps the penalized entries apart: ready values in
   // fcum, positions at the top of fpos (k + 2 |list| < lcap: no overlap)
-  const bool fast = nsel <= 1024u;
+  // rank merge (O(nsel^2 / NT) compares per thread) for short candidate lists;
+  // longer ones (long penalty lists: kp = k + |list|) take the radix cut +
+  // register sort of one warp
+#ifndef DP_RANK_MAX_ITERS
+#define DP_RANK_MAX_ITERS 48
+#endif
+  const bool fast = nsel * nsel <= (uint32_t)DP_RANK_MAX_ITERS * NT;
   double m_sub = 0.0, m_add = 0.0;
   for (int32_t j = t; j < plen; j += NT) {
     int32_t pos, c;
@@ -518,7 +524,7 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
     lap(13);
     // canonical order (ready desc, position asc): one warp through registers
     // for short lists, all NT threads in shared memory otherwise
-    if (p2 <= 256) {
+    if (p2 <= 256 || k <= 64) {   // warp_topk_sort cuts any list to the top k <= 64 first
       if (warp == 0) {
         warp_topk_sort(fkey, fpos, nl, (uint32_t)k, hash);
         const uint32_t m = min((uint32_t)k, nl);

@@ -8,6 +8,14 @@
 namespace dp {
 
 enum Mode : int { kFull = 0, kHot = 1, kTail = 2 };
+// Admission threshold estimate of the streaming top-k kernels: the first
+// batch's sample estimates the (kEstOver * kp)-th largest of the segment.  A
+// too-high estimate (fewer than kp admitted) costs a whole re-stream, which
+// long penalty lists (kp = k + |list| ~ 200) made frequent at 2x.
+#ifndef DP_EST_OVER
+#define DP_EST_OVER 4.0f
+#endif
+constexpr float kEstOver = DP_EST_OVER;
 constexpr int kMaxShards = 8;
 
 struct SampleArgs {

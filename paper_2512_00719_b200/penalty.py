@@ -144,6 +144,23 @@ class PenaltyState:
         if not _capturing():
             self._replayed = False
 
+    def select(self, rows) -> None:
+        """Keep only `rows` (int64 device/host index, batch order kept): the
+        table side of retiring finished sequences at an iteration boundary
+        (service.py:709-714).  Device gathers, no host copy of the table."""
+        import torch
+
+        idx = torch.as_tensor(rows, dtype=torch.int64, device=self.device)
+        self.ids = self.ids.index_select(0, idx).contiguous()
+        self.out_count = self.out_count.index_select(0, idx).contiguous()
+        self.len = self.len.index_select(0, idx).contiguous()
+        self.prompt_len = self.prompt_len.index_select(0, idx).contiguous()
+        self.batch = int(idx.numel())
+        self._native.ids = self.ids.data_ptr()
+        self._native.out_count = self.out_count.data_ptr()
+        self._native.len = self.len.data_ptr()
+        self._native.prompt_len = self.prompt_len.data_ptr()
+
     def rows(self):
         """Host copy: list of (ids, out_counts) per row (debug / parity tests)."""
         n = self.len.cpu().numpy()

@@ -419,6 +419,60 @@ class DecisionPlane:
                    _ptr(out), _stream(self.device))
         return out
 
+    # -- sequence lifecycle (service.py:709-714) --------------------------------
+    def mark_eos(self, d: Decisions, eos_ids) -> None:
+        """Set DP_FLAG_EOS on every row whose token is an end-of-sequence id
+        (TokenDecision.is_eos; carried by dp_encode_decisions), on device."""
+        import torch
+
+        if not eos_ids:
+            return
+        with torch.cuda.device(self.device):
+            key = tuple(sorted(int(e) for e in eos_ids))
+            if getattr(self, "_eos_key", None) != key:
+                self._eos_key, self._eos_dev = key, torch.tensor(key, dtype=torch.int32, device=self.device)
+            hit = torch.isin(d.token, self._eos_dev)
+            d.flags.bitwise_or_(hit.to(torch.uint8) * N.FLAG_EOS)
+
+    def select_rows(self, rows) -> None:
+        """Keep only `rows` of the batch (in order): params, seq ids, penalty
+        table and scratch follow; the hot set is shared.  Lands between
+        iterations, like the reference's active-list update."""
+        import torch
+
+        rows = np.asarray(rows, dtype=np.int64)
+        if rows.ndim != 1 or (rows.size and (rows.min() < 0 or rows.max() >= self.batch)):
+            raise ValueError("rows must index the current batch")
+        with torch.cuda.device(self.device):
+            self.seq_ids = self.seq_ids[rows]
+            self._seq_dev = torch.from_numpy(self.seq_ids.view(np.int64).copy()).to(self.device)
+            self.state.select(torch.from_numpy(rows).to(self.device))
+            self.batch = int(rows.size)
+            wl = int(N.load().dp_workspace_len(self.batch))
+            self._workspace = torch.zeros(wl, dtype=torch.int32, device=self.device)
+            self.set_params([self.params[i] for i in rows.tolist()])
+            self._out = {}
+            self._scratch = torch.empty(self.batch + 1, dtype=torch.int32, device=self.device)
+
+    def retire_finished(self, d: Decisions, eos_ids=frozenset(), max_tokens: int | None = None) -> np.ndarray:
+        """The reference's retirement rule (service.py:709-714): drop every
+        row whose token is an EOS id or whose sequence reached `max_tokens`
+        generated tokens; returns the kept row indices (of the batch before
+        the call).  Synchronises once (the new batch size is a host value)."""
+        import torch
+
+        with torch.cuda.device(self.device):
+            keep = torch.ones(self.batch, dtype=torch.bool, device=self.device)
+            if eos_ids:
+                self.mark_eos(d, eos_ids)
+                keep &= (d.flags & N.FLAG_EOS) == 0
+            rows = torch.nonzero(keep).flatten().cpu().numpy()
+        if max_tokens is not None and self.state.recorded >= int(max_tokens):
+            rows = rows[:0]
+        if rows.size != self.batch:
+            self.select_rows(rows)
+        return rows
+
     def to_decisions(self, d: Decisions, iteration: int, eos_ids=frozenset(), raise_degenerate: bool = True):
         """Host TokenDecision list (core.py:172-181); synchronises.
 

@@ -132,3 +132,39 @@ def test_bytes_touched_per_row(torch_cuda, bf16):
     algo = h * esz + rej.mean() * (v - h) * esz
     assert algo <= bt.mean() <= 1.5 * algo + plen.mean() * esz * 3
     print(f"SHVS bytes/row: measured {bt.mean():.0f}, algorithmic {algo:.0f}, reject {rej.mean():.3f}")
+
+
+def test_eos_retirement_compacts_rows_and_keeps_decisions(torch_cuda):
+    """service.py:709-714: rows whose token is an EOS id leave the batch at
+    the iteration boundary.  The compacted plane keeps each surviving row's
+    seq_id, params and penalty list, so its next decisions equal those of a
+    plane that never retired anyone (uniforms are keyed by seq_id)."""
+    torch = torch_cuda
+    from paper_2512_00719_b200 import DecisionPlane, SamplingParams, _native as N
+    from paper_2512_00719_b200.synthetic import SyntheticSource
+
+    v, bsz = 4096, 64
+    prompts = [np.random.default_rng(b).integers(0, v, 16) for b in range(bsz)]
+    params = [SamplingParams(**C2, seed=b) for b in range(bsz)]
+    a = DecisionPlane(v, params, prompts=prompts, seq_ids=np.arange(100, 100 + bsz))
+    ref = DecisionPlane(v, params, prompts=prompts, seq_ids=np.arange(100, 100 + bsz))
+    src = SyntheticSource(v, device="cuda")
+    x0 = src.generate(0, range(100, 100 + bsz))
+    d = a.sample(x0, 0)
+    r0 = ref.sample(x0, 0)
+    tok0 = d.token.cpu().numpy()
+    eos = {int(tok0[3]), int(tok0[10])}
+    kept = a.retire_finished(d, eos)
+    fl = d.flags.cpu().numpy()
+    assert all(bool(fl[b] & N.FLAG_EOS) == (int(tok0[b]) in eos) for b in range(bsz))
+    assert 3 not in kept and 10 not in kept and a.batch == kept.size
+    assert np.array_equal(a.seq_ids, np.arange(100, 100 + bsz)[kept])
+    x1 = src.generate(1, range(100, 100 + bsz))
+    d1 = a.sample(x1[torch.from_numpy(kept).cuda()].contiguous(), 1)
+    r1 = ref.sample(x1, 1)
+    assert np.array_equal(d1.token.cpu().numpy(), r1.token.cpu().numpy()[kept])
+    rows_a, rows_r = a.state.rows(), ref.state.rows()
+    for i, b in enumerate(kept):
+        assert np.array_equal(rows_a[i][0], rows_r[b][0]) and np.array_equal(rows_a[i][1], rows_r[b][1])
+    # max_tokens: everything retires once the generated length is reached
+    assert a.retire_finished(d1, max_tokens=2).size == 0 and a.batch == 0

@@ -9,5 +9,6 @@ run c2_shvs --config c2 --variant shvs --steps 500 --warmup 5 --no-cpu-baseline
 run c1 --config c1 --steps 1000 --warmup 10 --no-cpu-baseline
 run c3 --config c3 --steps 300 --warmup 5 --no-cpu-baseline
 run c5 --config c5 --steps 50 --warmup 3 --no-cpu-baseline
+run c5_full --config c5 --variant full --steps 30 --warmup 3 --no-cpu-baseline --no-shvs
 run c4 --config c4 --steps 50 --warmup 3 --no-cpu-baseline
 run ref --impl reference --steps 5 --warmup 3

@@ -13,6 +13,7 @@ from paper_2512_00719_b200.synthetic import SyntheticSource
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c2")
 ap.add_argument("--out", default=None)
+ap.add_argument("--grow", type=int, default=0, help="decide (and record) this many steps first: longer penalty lists")
 args = ap.parse_args()
 cfg = bench.CONFIGS[args.config]
 v, b = cfg["V"], cfg["B"]
@@ -21,6 +22,8 @@ src = SyntheticSource(v, device="cuda")
 plane = DecisionPlane(v, [bench.row_params(cfg, s) for s in range(b)], prompts=prompts, max_generated=136)
 dt = torch.bfloat16 if cfg["dtype"] == "bf16" else torch.float32
 xs = [src.generate(i, range(b), dtype=dt) for i in range(2)]
+for i in range(args.grow):
+    plane.sample(xs[i & 1], 1000 + i)
 for i in range(4):
     d = plane.sample(xs[i & 1], i, debug=True, topk_stride=8, update=False)
 torch.cuda.synchronize()

@@ -6,17 +6,18 @@ TAG=${1:-ncu}
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 O=gpurun_out/$TAG; mkdir -p $O
 NCU="ncu --set full --clock-control none --import-source on"
-cap() {   # name kernel-regex skip args...
+cap() {   # name kernel-regex (on the mangled name) skip args...
   local name=$1 k=$2 s=$3; shift 3
-  timeout 300 $NCU -k regex:$k -s $s -c 1 -o $O/$name python tools/prof_step.py "$@" > $O/$name.log 2>&1
+  timeout 300 $NCU --kernel-name-base mangled -k regex:$k -s $s -c 1 -o $O/$name python tools/prof_step.py "$@" \
+    > $O/$name.log 2>&1
 }
 cap k1p_c2      topk_persist   1 --config c2 --steps 3
 cap k1_c4       topk_sample    1 --config c4 --steps 2
 cap k1w_hot_c2  warp_sample    1 --config c2 --variant shvs --hot 2048 --steps 3
-cap k1_tail_c2  'topk_sample.*Li2E' 1 --config c2 --variant shvs --hot 2048 --steps 3
+cap k1_tail_c2  'topk_sample_kernelIfLi2E' 1 --config c2 --variant shvs --hot 2048 --steps 3
 cap k1b_c2n     general_sample 1 --config c2n --steps 3
-cap k2_raw_c2   'row_summary_kernel.*Lb0E' 0 --config c2 --variant shvs --hot 2048 --steps 1
-cap k2_pen_c2   'row_summary_kernel.*Lb1E' 0 --config c2 --variant shvs --hot 2048 --steps 1 --extra summary
+cap k2_raw_c2   'row_summary_kernelIfLi256ELi4ELb0E' 0 --config c2 --variant shvs --hot 2048 --steps 1
+cap k2_pen_c2   'row_summary_kernelIfLi256ELi4ELb1E' 0 --config c2 --variant shvs --hot 2048 --steps 1 --extra summary
 cap k6_c2       hot_mass_curve 0 --config c2 --variant shvs --hot 32768 --steps 1 --extra curve
 cap synth_fused synth_summary  0 --config c2 --variant shvs --hot 2048 --steps 1 --extra fused
 cap k1w_hot_c5  warp_sample    1 --config c5 --variant shvs --hot 2048 --steps 2

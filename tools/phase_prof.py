@@ -23,6 +23,7 @@ ap.add_argument("--variant", default="shvs")
 ap.add_argument("--hot", type=int, default=4096)
 ap.add_argument("--kernel", type=int, default=0)
 ap.add_argument("--steps", type=int, default=4)
+ap.add_argument("--grow", type=int, default=0, help="decide (and record) this many steps first: longer penalty lists")
 args = ap.parse_args()
 cfg = bench.CONFIGS[args.config]
 v, b = cfg["V"], cfg["B"]
@@ -35,6 +36,11 @@ perm = hot.device_maps(plane.device)[0] if hot is not None else None
 dt = torch.bfloat16 if cfg["dtype"] == "bf16" else torch.float32
 x = src.generate(0, range(b), dtype=dt, perm=perm)
 summ = plane.producer_summary(x) if args.variant == "shvs" else None
+for i in range(args.grow):
+    if args.variant == "shvs":
+        plane.sample(x, 1000 + i, variant="shvs", summary=summ, summary_raw=True)
+    else:
+        plane.sample(x, 1000 + i)
 for i in range(args.steps):
     d = plane._outputs(True, 0)
     d.stats.zero_()
