@@ -18,7 +18,7 @@ PKG = os.path.join(ROOT, "paper_2512_00719_b200")
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIBDIR, "libdecplane_b200.so")
-SOURCES = ["capi.cu", "sample_topk.cu", "sample_warp.cu", "sample_general.cu", "summary.cu", "aux_kernels.cu", "collective.cu"]
+SOURCES = ["capi.cu", "sample_topk.cu", "sample_warp.cu", "sample_general.cu", "summary.cu", "aux_kernels.cu", "collective.cu", "sample_persist.cu", "sample_hot.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

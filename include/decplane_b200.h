@@ -127,6 +127,12 @@ typedef struct {
 #define DP_PLAN_NO_PERSIST 0x2
 /* dp_sample_full: use K1p whenever its rows allow (tests) */
 #define DP_PLAN_FORCE_PERSIST 0x4
+/* dp_sample_shvs with H <= 4096: the exact-sort hot pass K1h decides the
+ * nucleus rows (top-k off) instead of the streaming kernels' 256-entry list +
+ * general-kernel fallback (measured slower at H = 2,048: opt-in) */
+#define DP_PLAN_HOT_SORT 0x8
+/* ... and every hot row (tests) */
+#define DP_PLAN_HOT_SORT_ALL 0x10
 
 typedef struct {
   int32_t max_top_k;

@@ -25,6 +25,8 @@ FLAG_DEGENERATE = 0x80
 PLAN_FORCE_RESUM = 0x1
 PLAN_NO_PERSIST = 0x2
 PLAN_FORCE_PERSIST = 0x4
+PLAN_HOT_SORT = 0x8
+PLAN_HOT_SORT_ALL = 0x10
 
 EXPORTS = [
     "dp_version", "dp_device_check", "dp_last_error", "dp_uniforms", "dp_sample_full",

@@ -16,6 +16,7 @@ cudaError_t launch_warp(const SampleArgs& a, int dtype, int mode, int grid_rows,
 int persist_grid(const SampleArgs& a, int dtype);
 size_t persist_smem_bytes(const SampleArgs& a);
 cudaError_t launch_persist(const SampleArgs& a, int dtype, int grid, cudaStream_t st);
+cudaError_t launch_hot_sort(const SampleArgs& a, int dtype, cudaStream_t st);
 cudaError_t launch_row_summary(const void* logits, int dtype, int64_t B, int64_t V, int64_t ld,
                                const dp_params_t* params, const dp_penalty_t& pen, const int32_t* inv_perm,
                                double* row_max, double* total, cudaStream_t st);
@@ -113,7 +114,9 @@ Launches plan_launches(dp::SampleArgs& a, const dp_plan_t* plan, int mode, int64
   Launches L;
   const int kernel = plan ? plan->kernel : 0;
   const int64_t kmax = plan ? plan->max_top_k : 0, kmin = plan ? plan->min_top_k : 0;
-  const bool bounded = kmax > 0 && kmin > 0 && kmax < n;
+  // kHot with K1h taking the nucleus rows: the top-k rows are bounded by kmax alone
+  const bool nuc_elsewhere = a.use_hot_sort == 1 && mode == dp::kHot;
+  const bool bounded = kmax > 0 && (kmin > 0 || nuc_elsewhere) && kmax < n;
   const int64_t cap = dp::pen_bound(a.pen);
   a.use_warp = 0;
   if (mode != dp::kTail && kernel != 1) {
@@ -462,20 +465,38 @@ int sample_shvs_impl(const void* logits, int dtype, int64_t B, int64_t V, int64_
     a.force_resum = (plan_host->flags & DP_PLAN_FORCE_RESUM) ? 1 : 0;
     if ((e = cudaMemsetAsync(rl, 0, sizeof(int32_t), st)) != cudaSuccess) return cuda_status(e, "dp_sample_shvs/memset");
   }
-  // hot pass over [0, H)
+  // hot pass over [0, H): short hot sets by the exact sort (K1h), longer ones
+  // by the streaming kernels
   plan_topk(a, plan_host, B, H, dtype == DP_F32 ? 4 : 2);
   fit_topk(a, dp::kHot);
-  const bool nuc = nucleus_possible(plan_host) && arm_fallback(a, plan_host, 1, B, st, e);
-  if (e != cudaSuccess) return cuda_status(e, "dp_sample_shvs/fallback");
-  const Launches L = plan_launches(a, plan_host, dp::kHot, B, H);
-  if (L.warp && (e = dp::launch_warp(a, dtype, dp::kHot, (int)B, st)) != cudaSuccess)
-    return cuda_status(e, "dp_sample_shvs/hot-warp");
-  if (L.topk && (e = dp::launch_topk(a, dtype, dp::kHot, (int)B, st)) != cudaSuccess)
-    return cuda_status(e, "dp_sample_shvs/hot-topk");
-  if (L.general && (e = dp::launch_general(a, dtype, dp::kHot, (int)B, st)) != cudaSuccess)
-    return cuda_status(e, "dp_sample_shvs/hot-general");
-  if (nuc && (e = launch_fallback(a, dtype, dp::kHot, B, st)) != cudaSuccess)
-    return cuda_status(e, "dp_sample_shvs/hot-fallback");
+  const int kern = plan_host ? plan_host->kernel : 0;
+  const int pf = plan_host ? plan_host->flags : 0;
+  const bool hot_sort = H <= dp::kHotSortMax && kern != 1 && kern != 2 &&
+                        (pf & (DP_PLAN_HOT_SORT | DP_PLAN_HOT_SORT_ALL));
+  const bool sort_all = hot_sort && (pf & DP_PLAN_HOT_SORT_ALL);
+  a.use_hot_sort = sort_all ? 2 : (hot_sort ? 1 : 0);
+  // nucleus rows (top-k off) go to K1h when it is on: the streaming kernels
+  // then only see top-k rows and need no nucleus list / fallback
+  const bool nuc_rows = nucleus_possible(plan_host);
+  if (a.use_hot_sort && (nuc_rows || sort_all)) {
+    if ((e = dp::launch_hot_sort(a, dtype, st)) != cudaSuccess) return cuda_status(e, "dp_sample_shvs/hot-sort");
+  }
+  bool nuc = false;
+  const bool any_stream_rows = !sort_all && !(a.use_hot_sort && plan_host && plan_host->max_top_k <= 0);
+  if (any_stream_rows) {
+    if (!a.use_hot_sort) nuc = nuc_rows && arm_fallback(a, plan_host, 1, B, st, e);
+    if (e != cudaSuccess) return cuda_status(e, "dp_sample_shvs/fallback");
+    const Launches L = plan_launches(a, plan_host, dp::kHot, B, H);
+    if (L.warp && (e = dp::launch_warp(a, dtype, dp::kHot, (int)B, st)) != cudaSuccess)
+      return cuda_status(e, "dp_sample_shvs/hot-warp");
+    if (L.topk && (e = dp::launch_topk(a, dtype, dp::kHot, (int)B, st)) != cudaSuccess)
+      return cuda_status(e, "dp_sample_shvs/hot-topk");
+    if (L.general && (e = dp::launch_general(a, dtype, dp::kHot, (int)B, st)) != cudaSuccess)
+      return cuda_status(e, "dp_sample_shvs/hot-general");
+    if (nuc && (e = launch_fallback(a, dtype, dp::kHot, B, st)) != cudaSuccess)
+      return cuda_status(e, "dp_sample_shvs/hot-fallback");
+  }
+  nuc = nucleus_possible(plan_host);   // the tail pass may hold nucleus rows either way
   if (H == V) return DP_OK;
   if (resum && (e = dp::launch_resum(a, dtype, st)) != cudaSuccess) return cuda_status(e, "dp_sample_shvs/resum");
   // tail pass over [H, V) for the rows the hot pass rejected

@@ -16,6 +16,7 @@ enum Mode : int { kFull = 0, kHot = 1, kTail = 2 };
 #define DP_EST_OVER 4.0f
 #endif
 constexpr float kEstOver = DP_EST_OVER;
+constexpr int kHotSortMax = 4096;   // SHVS hot prefixes up to this size take K1h (sample_hot.cu)
 constexpr int kMaxShards = 8;
 
 struct SampleArgs {
@@ -63,6 +64,7 @@ struct SampleArgs {
   int32_t* resum_count;
   double* resum_sh;             // [B] the row's hot mass S_H (relative to row_max)
   int32_t force_resum;          // DP_PLAN_FORCE_RESUM (test hook)
+  int32_t use_hot_sort;         // kHot: 1 = nucleus rows go to K1h (sample_hot.cu), 2 = every row
 };
 
 // upper bound of the penalty-list length over the call's rows (sizes lists)
@@ -183,7 +185,7 @@ DP_DEV void thread_record_token(const SampleArgs& a, int row, int32_t tok) {
 //  * warp-per-row kernel (short top-k, sample_warp.cu) when the call uses it;
 //  * per-row CTA / cluster streaming top-k kernel (sample_topk.cu);
 //  * general radix kernel (no top-k / oversized lists, sample_general.cu).
-enum Route : int { kRouteGeneral = 0, kRouteTopk = 1, kRouteWarp = 2 };
+enum Route : int { kRouteGeneral = 0, kRouteTopk = 1, kRouteWarp = 2, kRouteHotSort = 3 };
 // Rows with top-k off (top-p only, min-p only, neutral) take the top-k kernel
 // as "nucleus" rows: it keeps the exact kNucK largest ready values plus the
 // mass of the whole domain, and decides the row when the kept set (and the
@@ -203,6 +205,7 @@ DP_DEV bool warp_row_ok(const SampleArgs& a, int32_t k, int32_t plen, int64_t n)
          plen <= kWarpPenCap;
 }
 DP_DEV int route_row(const SampleArgs& a, int mode, int32_t k, int32_t plen, int64_t n) {
+  if (mode == kHot && (a.use_hot_sort == 2 || (a.use_hot_sort == 1 && nucleus_row(k, n)))) return kRouteHotSort;
   if (a.force_general) return kRouteGeneral;
   if (a.use_warp && warp_row_ok(a, k, plen, n)) return kRouteWarp;
   if (nucleus_row(k, n)) {

@@ -110,6 +110,7 @@ class DecisionPlane:
             self.hot = hot
             self.split = int(split)
             self.kernel = int(kernel)   # dp_plan_t.kernel: 0 auto, 1 CTA/cluster, 2 warp-per-row
+            self.plan_flags = 0         # extra DP_PLAN_* bits (A-B / test hooks)
             # caller-owned library scratch (fallback row lists): one per plane
             wl = int(N.load().dp_workspace_len(self.batch))
             self._workspace = torch.zeros(wl, dtype=torch.int32, device=self.device)
@@ -224,7 +225,7 @@ class DecisionPlane:
                     summary = self.row_summary(logits, inv_perm=inv)   # exact, penalized
                 rmax, tot = summary
                 self._plan.summary_raw = 1 if summary_raw else 0
-                self._plan.flags = N.PLAN_FORCE_RESUM if force_resum else 0   # test hook
+                self._plan.flags = self.plan_flags | (N.PLAN_FORCE_RESUM if force_resum else 0)   # test hooks
                 pen = self.state.prepare(update)
                 N.call("dp_sample_shvs", _ptr(logits), dt, self.batch, self.vocab_size, self.hot.size,
                        logits.stride(0), _ptr(perm), _ptr(inv), _ptr(rmax), _ptr(tot), _ptr(self._params_dev),
@@ -314,7 +315,7 @@ class DecisionPlane:
             rmax, tot = summary
             self._plan.summary_raw = 1 if summary_raw else 0
             self._plan.fuse_update = 1 if update else 0
-            self._plan.flags = 0
+            self._plan.flags = self.plan_flags
             pen = self.state.prepare(update)
             N.call("dp_sample_shvs_split", _ptr(hot), hot.stride(0), _ptr(tail), tail.stride(0), dt, self.batch,
                    self.vocab_size, h, _ptr(perm), _ptr(inv), _ptr(rmax), _ptr(tot), _ptr(self._params_dev),

@@ -42,7 +42,7 @@ def plane_for(torch, vocab, params, prompts, hot_ids=None, max_generated=65536, 
 
 
 # dp_plan_t.kernel: 1 = per-row CTA / cluster kernel, 2 = warp-per-row kernel
-KERNELS = [1, 2]
+KERNELS = [0, 1, 2]   # 0: auto
 
 
 def compare(tag, gpu_tok, gpu_lp, dec, exempt_log, lp_tol=1e-7):
@@ -60,11 +60,16 @@ def compare(tag, gpu_tok, gpu_lp, dec, exempt_log, lp_tol=1e-7):
 
 
 def run_golden(torch, name, variant, raw_summary=False, kernel=0, storage="whole", force_resum=False):
+    from paper_2512_00719_b200 import _native as N
+
     case = Case(name)
     params = case.params()
     states = case.states()
+    # the exact-sort hot pass K1h: "sortall" every row, "sortnuc" the rows without top-k
+    sort = {"sortall": N.PLAN_HOT_SORT_ALL, "sortnuc": N.PLAN_HOT_SORT}.get(kernel, 0)
     plane = plane_for(torch, case.vocab, params, [case.prompts[b] for b in range(case.batch)],
-                      hot_ids=case.hot_ids, kernel=kernel)
+                      hot_ids=case.hot_ids, kernel=0 if sort else kernel)
+    plane.plan_flags = sort
     exempt = []
     resummed = 0
     for it in range(case.iters):
@@ -162,13 +167,13 @@ def test_full_path_matches_reference_run(torch_cuda, name, kernel):
     run_golden(torch_cuda, name, "full", kernel=kernel)
 
 
-@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("kernel", KERNELS + ["sortall", "sortnuc"])
 @pytest.mark.parametrize("name", ["shvs_accept", "shvs_reject", "het_shvs", "shvs_neutral"])
 def test_shvs_matches_reference_run(torch_cuda, name, kernel):
     run_golden(torch_cuda, name, "shvs", kernel=kernel)
 
 
-@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("kernel", KERNELS + ["sortall"])
 @pytest.mark.parametrize("name", ["shvs_accept", "shvs_reject", "het_shvs"])
 def test_shvs_with_producer_raw_summary(torch_cuda, name, kernel):
     """SHVS fed the producer's penalty-free summary, corrected on device for
