@@ -46,6 +46,9 @@ CONFIGS = {
     "c2p": dict(V=152064, B=1024, dtype="f32", params=dict(temperature=0.8, top_p=0.9), name="c2-top-p-only"),
     "c2m": dict(V=152064, B=1024, dtype="f32", params=dict(temperature=0.8, min_p=0.05), name="c2-min-p-only"),
     "c2n": dict(V=152064, B=1024, dtype="f32", params=dict(temperature=0.8), name="c2-neutral"),
+    # C2 with 2,048-token prompts per row (~2,000 unique penalized ids: the
+    # realistic serving penalty state)
+    "c2long": dict(V=152064, B=1024, dtype="f32", params=C2_PARAMS, name="c2-2048-token-prompts", prompt_len=2048),
 }
 METRIC = "sampled tokens/s at V=152k, B=1024; achieved HBM GB/s vs B200 peak"
 PROMPT_LEN = 32
@@ -275,7 +278,7 @@ def reference_arm(args, cfg):
     nrows = int(min(cfg["B"], max(64, len(os.sched_getaffinity(0)))))
     src = O.Synthetic(v)
     x = src.wire(0, range(nrows))
-    prompts = [np.random.default_rng(b).integers(0, v, PROMPT_LEN) for b in range(nrows)]
+    prompts = [np.random.default_rng(b).integers(0, v, cfg.get("prompt_len", PROMPT_LEN)) for b in range(nrows)]
     steps = []
     # bounded: the whole --steps K --warmup W run stays within ~ref_budget
     # seconds (one process pool; every step decides each process's rows at
@@ -545,7 +548,7 @@ def run_ours(args, cfg):
     shard = BatchShard(cfg["B"] if scaling == "strong" else cfg["B"] * world, world, rank)
     b_local = shard.rows
     seq_ids = shard.seq_ids
-    prompts = [np.random.default_rng(int(s)).integers(0, v, PROMPT_LEN) for s in seq_ids]
+    prompts = [np.random.default_rng(int(s)).integers(0, v, cfg.get("prompt_len", PROMPT_LEN)) for s in seq_ids]
     params = [row_params(cfg, int(s)) for s in seq_ids]
     src = SyntheticSource(v, device=dev)
     variant = args.variant or ("shvs" if cfg.get("mix") else "full")

@@ -126,15 +126,19 @@ Launches plan_launches(dp::SampleArgs& a, const dp_plan_t* plan, int mode, int64
   // every row with top-k on fits the warp kernel / the top-k kernel
   const bool all_warp = a.use_warp && bounded && kmax <= dp::kWarpKMax && cap <= dp::kWarpPenCap &&
                         (kmax + cap <= dp::kWarpKpMax || n <= dp::kWarpKpMax);
-  const int64_t kp_topk = kmax + (mode == dp::kHot ? 0 : cap);
-  const bool k_rows_fit = kmax > 0 && kmax < n && (kp_topk < n ? kp_topk : n) <= a.kcap && kmax + 2 * cap <= a.lcap;
+  // penalized ids outside the stream (kHot, long lists): kp = k, and the
+  // final stage keeps at most kPenSelCap penalized entries
+  const bool excl = mode == dp::kHot || a.pen_excl;
+  const int64_t pl = (excl && cap > dp::kPenSelCap) ? dp::kPenSelCap : cap;
+  const int64_t kp_topk = kmax + (excl ? 0 : cap);
+  const bool k_rows_fit = kmax > 0 && kmax < n && (kp_topk < n ? kp_topk : n) <= a.kcap && kmax + 2 * pl <= a.lcap;
   const bool all_topk = bounded && k_rows_fit;
   // top-k-off rows present (kmin == 0): they are nucleus rows of the top-k
   // kernel (the general kernel then only sees the fallback list) when the
   // nucleus list fits; rows with top-k on fit by k_rows_fit
-  const int64_t kp_nuc = dp::kNucK + (mode == dp::kHot ? 0 : cap);
+  const int64_t kp_nuc = dp::kNucK + (excl ? 0 : cap);
   const bool nuc_all = a.fb_rows != nullptr && n >= 2 * (int64_t)dp::kNucK && kp_nuc <= a.kcap &&
-                       dp::kNucK + 2 * cap <= a.lcap;
+                       dp::kNucK + 2 * pl <= a.lcap;
   const bool mixed_topk = kmin == 0 && k_rows_fit && nuc_all;
   L.warp = a.use_warp != 0;
   L.topk = !all_warp;
@@ -178,10 +182,17 @@ int persist_grid_cached(const dp::SampleArgs& a, int dtype) {
 }
 
 // capacities for the streaming top-k kernel (see sample_topk.cu)
-void plan_topk(dp::SampleArgs& a, const dp_plan_t* plan, int64_t B, int64_t n, int elem_bytes) {
+void plan_topk(dp::SampleArgs& a, const dp_plan_t* plan, int64_t B, int64_t n, int elem_bytes, int mode) {
   int32_t kmax = (plan && plan->max_top_k > 0) ? plan->max_top_k : 256;
   if (nucleus_possible(plan) && kmax < dp::kNucK) kmax = dp::kNucK;   // nucleus rows keep kNucK
-  const uint32_t kcap = pow2_at_least((uint32_t)kmax + (uint32_t)dp::pen_bound(a.pen));
+  // long penalty lists: the streaming selection excludes the penalized ids
+  // (shared bitmap) instead of widening to k + |list|, and the final stage
+  // keeps only the best kPenSelCap penalized entries (finish.cuh)
+  const int32_t pb = dp::pen_bound(a.pen);
+  a.pen_excl = (mode != dp::kHot && a.nshard == 0 && pb > dp::kPenExclMin) ? 1 : 0;
+  const bool excl = mode == dp::kHot || a.pen_excl;
+  const int32_t pl = (excl && pb > dp::kPenSelCap) ? dp::kPenSelCap : pb;
+  const uint32_t kcap = pow2_at_least((uint32_t)kmax + (uint32_t)(a.pen_excl ? 0 : pb));
   a.kcap = (int32_t)(kcap < 32u ? 32u : kcap);
   if (a.kcap > 2048) a.kcap = 2048;
   // vector slots of the streaming stage's candidate buffer (wcap field): the
@@ -189,7 +200,7 @@ void plan_topk(dp::SampleArgs& a, const dp_plan_t* plan, int64_t B, int64_t n, i
   // handled exactly (re-stream), so this only sizes the common case
   a.wcap = (int32_t)(4u * (uint32_t)a.kcap > 1024u ? 4u * (uint32_t)a.kcap : 1024u);
   if (a.wcap > 4096) a.wcap = 4096;
-  a.lcap = (int32_t)pow2_at_least((uint32_t)kmax + 2u * (uint32_t)dp::pen_bound(a.pen) + 1u);
+  a.lcap = (int32_t)pow2_at_least((uint32_t)kmax + 2u * (uint32_t)pl + 1u);
   if (a.lcap > 4096) a.lcap = 4096;
   int split = plan && plan->split > 0 ? plan->split : 0;
   if (split == 0) {
@@ -275,7 +286,7 @@ int dp_sample_full(const void* logits, int dtype, int64_t B, int64_t V, int64_t 
   a.logprob = logprob;
   a.flags = flags;
   if (debug_host) a.dbg = *debug_host;
-  plan_topk(a, plan_host, B, V, dtype == DP_F32 ? 4 : 2);
+  plan_topk(a, plan_host, B, V, dtype == DP_F32 ? 4 : 2, dp::kFull);
   fit_topk(a, dp::kFull);
   cudaError_t e = cudaSuccess;
   const bool nuc = nucleus_possible(plan_host) && arm_fallback(a, plan_host, 0, B, st, e);
@@ -287,7 +298,8 @@ int dp_sample_full(const void* logits, int dtype, int64_t B, int64_t V, int64_t 
     // several waves of rows with top-k only: the persistent warp-specialised
     // K1p overlaps each row's final stage with the next row's stream
     const bool no_persist = plan_host && (plan_host->flags & DP_PLAN_NO_PERSIST);
-    const int pg = (!no_persist && a.split == 1 && a.fb_rows == nullptr && !a.use_warp) ? persist_grid_cached(a, dtype)
+    const int pg = (!no_persist && a.split == 1 && a.fb_rows == nullptr && !a.use_warp && !a.pen_excl)
+                       ? persist_grid_cached(a, dtype)
                                                                                          : 0;
     if (std::getenv("DP_VERBOSE"))
       std::fprintf(stderr, "[dp] full: B=%lld persist_grid=%d smem=%zu topk_smem=%zu kcap=%d wcap=%d lcap=%d\n",
@@ -341,7 +353,8 @@ int dp_sample_full_sharded(const void* const* shards, int32_t t, int dtype, int6
   a.logprob = logprob;
   a.flags = flags;
   if (debug_host) a.dbg = *debug_host;
-  plan_topk(a, plan_host, B, V, dtype == DP_F32 ? 4 : 2);
+  a.nshard = t;   // (plan_topk: sharded rows keep the k + |list| selection)
+  plan_topk(a, plan_host, B, V, dtype == DP_F32 ? 4 : 2, dp::kFull);
   // one t-CTA cluster per row while the batch leaves SMs idle; otherwise the
   // fewest CTAs per row (a cluster rank's select + push is the per-CTA
   // overhead).  A CTA keeps <= 2 (EPV - 1) scalar head / tail keys per shard
@@ -467,7 +480,7 @@ int sample_shvs_impl(const void* logits, int dtype, int64_t B, int64_t V, int64_
   }
   // hot pass over [0, H): short hot sets by the exact sort (K1h), longer ones
   // by the streaming kernels
-  plan_topk(a, plan_host, B, H, dtype == DP_F32 ? 4 : 2);
+  plan_topk(a, plan_host, B, H, dtype == DP_F32 ? 4 : 2, dp::kHot);
   fit_topk(a, dp::kHot);
   const int kern = plan_host ? plan_host->kernel : 0;
   const int pf = plan_host ? plan_host->flags : 0;
@@ -511,7 +524,7 @@ int sample_shvs_impl(const void* logits, int dtype, int64_t B, int64_t V, int64_
     arm_fallback(t, plan_host, 2, B, st, e);
     if (e != cudaSuccess) return cuda_status(e, "dp_sample_shvs/fallback");
   }
-  plan_topk(t, plan_host, B, V - H, dtype == DP_F32 ? 4 : 2);
+  plan_topk(t, plan_host, B, V - H, dtype == DP_F32 ? 4 : 2, dp::kTail);
   // The tail pass serves only the rejected rows (typically a few percent of
   // B, count known on the device only): 4-CTA clusters split each row over 4
   // SMs, and the clusters loop over the reject list, so a handful of

@@ -355,21 +355,52 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
     }
   }
 
-  // penalized positions of this domain -> hash set (raw candidates defer to them)
-  // (kHot streamed around them already: no hash set needed)
+  // penalized positions of this domain -> hash set (raw candidates defer to
+  // them).  kHot, and long lists (a.pen_excl), streamed around the penalized
+  // ids already: no hash set needed
+  const bool excl = MODE == kHot || a.pen_excl;
   if (t == 0) {
     fs.nl = 0u;
     fs.np = 0u;
     fs.nq = 0u;
   }
-  if (MODE != kHot)
+  if (!excl)
     for (uint32_t i = t; i < hcap; i += NT) hash[i] = 0xFFFFFFFFu;
   sync();
   const bool nuc_mass = nuc && MODE != kHot;
   const float s2 = (float)(1.4426950408889634 / p.temperature);
   const double cref_r = (double)cref / p.temperature;   // cref in ready units
+  // Long lists with the penalized ids outside the stream: only the k best
+  // penalized entries (ties at the k-th value included) can enter the ready
+  // top-k, so only those are kept — a radix threshold over their exact f64
+  // keys, computed on the fly from the (L2-hot) list and logits.
+  uint64_t p_thr = 0ull;
+  const bool psel = excl && plen > kPenSelCap;
+  if (psel) {
+    auto get_p = [&](uint32_t j, uint64_t& key) -> bool {
+      int32_t pos, c;
+      float x;
+      pen_entry((int32_t)j, pos, x, c);
+      if (pos < 0) return false;
+      key = f64_key(ready_penalized(x, c, p));
+      return true;
+    };
+    uint32_t cv = 0;
+    for (int32_t j = t; j < plen; j += NT) {
+      uint64_t kk;
+      cv += get_p((uint32_t)j, kk) ? 1u : 0u;
+    }
+    cv = warp_sum(cv);
+    if (lane == 0) fs.wc[warp] = cv;
+    sync();
+    uint32_t cnt_p = 0;
+    for (int w = 0; w < NT / 32; ++w) cnt_p += fs.wc[w];
+    sync();
+    p_thr = group_select_threshold<NT>(get_p, (uint32_t)plen, cnt_p, (uint32_t)k, hash, fs.wc, t, sync);
+  }
+  const uint32_t pcap = F.cap - (uint32_t)k - 1u;   // penalized slots next to the k unpenalized ones
   // the rank-merge path keeps the penalized entries apart: ready values in
-  // fcum, positions at the top of fpos (k + 2 |list| < lcap: no overlap)
+  // fcum, positions at the top of fpos (k + 2 |kept list| < lcap: no overlap)
   // rank merge (O(nsel^2 / NT) compares per thread) for short candidate lists;
   // longer ones (long penalty lists: kp = k + |list|) take the radix cut +
   // register sort of one warp
@@ -383,19 +414,25 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
     float x;
     pen_entry(j, pos, x, c);
     if (pos >= 0) {
-      if (MODE != kHot) {
+      if (!excl) {
         uint32_t h = ((uint32_t)pos * 2654435761u) & hmask;
         while (atomicCAS(&hash[h], 0xFFFFFFFFu, (uint32_t)pos) != 0xFFFFFFFFu) h = (h + 1u) & hmask;
       }
       const double r = ready_penalized(x, c, p);
-      if (fast) {
-        const uint32_t s = atomicAdd(&fs.np, 1u);
-        fcum[s] = r;
-        fpos[F.cap - 1u - s] = (uint32_t)pos;
-      } else {
-        const uint32_t s = atomicAdd(&fs.nl, 1u);
-        fkey[s] = f64_key(r);
-        fpos[s] = (uint32_t)pos;
+      if (!psel || f64_key(r) >= p_thr) {
+        if (fast) {
+          const uint32_t s = atomicAdd(&fs.np, 1u);
+          if (s < pcap) {   // (ties at the k-th penalized value beyond kPenSelCap - k: not kept)
+            fcum[s] = r;
+            fpos[F.cap - 1u - s] = (uint32_t)pos;
+          }
+        } else {
+          const uint32_t s = atomicAdd(&fs.nl, 1u);
+          if (s < F.cap) {
+            fkey[s] = f64_key(r);
+            fpos[s] = (uint32_t)pos;
+          }
+        }
       }
       if (nuc_mass) {   // swap the streamed f32 term (bit-identical) for the exact one
         m_sub += (double)ex2_fast(((x - cref) - 0.f) * s2);
@@ -412,12 +449,17 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
     }
   }
   sync();
+  if (t == 0) {
+    if (fs.np > pcap) fs.np = pcap;
+    if (fs.nl > F.cap) fs.nl = F.cap;
+  }
+  sync();
   if (nuc_mass) {
     for (int w = 0; w < NT / 32; ++w) s_dom += fs.corr[w] - fs.sh_pen[w];   // fixed order
   }
   lap(12);
   auto penalized = [&](uint32_t pos) -> bool {
-    if (MODE == kHot || plen == 0) return false;
+    if (excl || plen == 0) return false;
     uint32_t h = (pos * 2654435761u) & hmask;
     while (true) {
       const uint32_t hv = hash[h];

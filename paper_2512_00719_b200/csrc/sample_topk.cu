@@ -99,7 +99,9 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
   extern __shared__ __align__(16) uint8_t smem[];
   const int64_t n = dom_n(a, MODE);
   const int64_t lo = dom_lo(a, MODE);
-  const uint32_t bm_words = MODE == kHot ? (uint32_t)((n + 31) / 32) + 1u : 0u;   // +1: vector window
+  // kHot, and long penalty lists (pen_excl), stream around the penalized ids
+  const bool excl = MODE == kHot || (MODE != kHot && a.pen_excl);
+  const uint32_t bm_words = excl ? (uint32_t)((n + 31) / 32) + 1u : 0u;   // +1: vector window
   const TopkLayout L = topk_layout<NT>(a.wcap, a.kcap, a.lcap, (int)bm_words, a.split);
   uint64_t* cand = reinterpret_cast<uint64_t*>(smem + L.cand);
   uint64_t* recv = reinterpret_cast<uint64_t*>(smem + L.recv);
@@ -135,7 +137,7 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
   const int32_t ke = nuc ? effective_k(k, n) : k;
   const bool nuc_mass = nuc && MODE != kHot;
   // kHot excludes penalized ids from the stream (bitmap) so it needs no widening
-  const uint32_t kp = (uint32_t)min64(n, (int64_t)ke + (MODE == kHot ? 0 : plen));
+  const uint32_t kp = (uint32_t)min64(n, (int64_t)ke + (excl ? 0 : plen));
   if (route_row(a, MODE, k, plen, n) != kRouteTopk) continue;   // another kernel's row (cluster-uniform)
 
 #ifdef DP_TIMELINE
@@ -166,13 +168,15 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
   double mrow = 0.0;
   float mtau_hi = 0.f, mtau_lo = 0.f;
   const float s2 = (float)(1.4426950408889634 / p.temperature);
-  if (MODE == kHot) {
+  if (excl) {
     for (uint32_t i = tid; i < bm_words; i += NT) bitmap[i] = 0u;
     __syncthreads();
     for (int32_t j = tid; j < plen; j += NT) {
       const int64_t pos = id_to_pos(a, pids[j]) - lo;
       if (pos >= 0 && pos < n) atomicOr(&bitmap[pos >> 5], 1u << (pos & 31));
     }
+  }
+  if (MODE == kHot) {
     mrow = a.row_max[row];
     const double c = mrow * p.temperature;
     mtau_hi = (float)c;
@@ -217,7 +221,7 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
   int32_t* cidx = reinterpret_cast<int32_t*>(cvec + ccap);      // their first element's row position
   const T* celem = reinterpret_cast<const T*>(cvec);
   auto pen_bit = [&](int64_t pos) -> bool {
-    return MODE == kHot && ((bitmap[pos >> 5] >> (pos & 31)) & 1u);
+    return excl && ((bitmap[pos >> 5] >> (pos & 31)) & 1u);
   };
 
   uint64_t thr = 0ull;     // admit keys >= thr
@@ -341,7 +345,7 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
 #pragma unroll
         for (int e = 0; e < EPV; ++e) {
           const float x = vec_elem<T>(v[j], e);
-          if (MODE != kHot || (idx < v_hi && !pen_bit((int64_t)a0 + (int64_t)idx * EPV + e))) mx = fmaxf(mx, x);
+          if (!excl || (idx < v_hi && !pen_bit((int64_t)a0 + (int64_t)idx * EPV + e))) mx = fmaxf(mx, x);
         }
       }
       const uint32_t kw = (kp + NW - 1) / NW;
@@ -604,7 +608,7 @@ static cudaError_t launch_topk_t(const SampleArgs& a, int grid_rows, cudaStream_
 #endif
   constexpr int U = DP_TOPK_U, NT = DP_TOPK_NT;
   const int64_t n = MODE == kFull ? a.V : (MODE == kHot ? a.H : a.V - a.H);
-  const int bm_words = MODE == kHot ? (int)((n + 31) / 32) + 1 : 0;
+  const int bm_words = (MODE == kHot || a.pen_excl) ? (int)((n + 31) / 32) + 1 : 0;
   const TopkLayout L = topk_layout<NT>(a.wcap, a.kcap, a.lcap, bm_words, a.split);
   auto kern = topk_sample_kernel<T, MODE, NT, U, NUC, SH>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
@@ -635,7 +639,7 @@ static cudaError_t launch_topk_m(const SampleArgs& a, int mode, int grid_rows, c
 // dynamic shared memory of a top-k launch with the call's capacities
 size_t topk_smem_bytes(const SampleArgs& a, int mode) {
   const int64_t n = mode == kFull ? a.V : (mode == kHot ? a.H : a.V - a.H);
-  const int bm_words = mode == kHot ? (int)((n + 31) / 32) + 1 : 0;
+  const int bm_words = (mode == kHot || a.pen_excl) ? (int)((n + 31) / 32) + 1 : 0;
   return topk_layout<DP_TOPK_NT>(a.wcap, a.kcap, a.lcap, bm_words, a.split).total;
 }
 

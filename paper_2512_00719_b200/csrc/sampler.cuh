@@ -65,7 +65,15 @@ struct SampleArgs {
   double* resum_sh;             // [B] the row's hot mass S_H (relative to row_max)
   int32_t force_resum;          // DP_PLAN_FORCE_RESUM (test hook)
   int32_t use_hot_sort;         // kHot: 1 = nucleus rows go to K1h (sample_hot.cu), 2 = every row
+  int32_t pen_excl;             // kFull / kTail: penalized ids leave the streaming selection
+                                //   (shared bitmap, kp = k) — long penalty lists (finish.cuh)
 };
+// penalty lists longer than this stream with the penalized ids excluded
+// (pen_excl) instead of widening the selection to k + |list|
+constexpr int kPenExclMin = 256;
+// the streaming kernel keeps at most this many penalized candidates per row
+// for its final merge (the best ones by ready value; finish.cuh)
+constexpr int kPenSelCap = 256;
 
 // upper bound of the penalty-list length over the call's rows (sizes lists)
 __host__ __device__ inline int32_t pen_bound(const dp_penalty_t& pen) {
@@ -212,8 +220,12 @@ DP_DEV int route_row(const SampleArgs& a, int mode, int32_t k, int32_t plen, int
     if (!a.fb_rows || (int64_t)kNucK * 2 > n) return kRouteGeneral;   // no fallback list / short domain
     k = kNucK;
   }
-  const uint32_t kp = (uint32_t)min64(n, (int64_t)k + (mode == kHot ? 0 : plen));
-  if (k > 0 && (int64_t)k < n && kp <= (uint32_t)a.kcap && (uint32_t)(k + 2 * plen) <= (uint32_t)a.lcap)
+  const bool excl = mode == kHot || a.pen_excl;
+  const uint32_t kp = (uint32_t)min64(n, (int64_t)k + (excl ? 0 : plen));
+  // the final stage holds k + 2 |list| entries, or (penalized ids excluded
+  // from the stream) at most the k + kPenSelCap best ones
+  const int32_t pl = (excl && plen > kPenSelCap) ? kPenSelCap : plen;
+  if (k > 0 && (int64_t)k < n && kp <= (uint32_t)a.kcap && (uint32_t)(k + 2 * pl) <= (uint32_t)a.lcap)
     return kRouteTopk;
   return kRouteGeneral;
 }

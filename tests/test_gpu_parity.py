@@ -706,12 +706,12 @@ def _bench_params(cfg_mix, b):
     return O.Params(**kw, seed=0)
 
 
-def _big_batch_parity(torch, v, bsz, bf16, mix, variant, hot_size, check_every, iters=2, raw=True):
+def _big_batch_parity(torch, v, bsz, bf16, mix, variant, hot_size, check_every, iters=2, raw=True, prompt_len=32):
     from paper_2512_00719_b200 import DecisionPlane, HotVocab, SamplingParams
     from paper_2512_00719_b200.synthetic import SyntheticSource
 
     params = [_bench_params(mix, b) for b in range(bsz)]
-    prompts = [np.random.default_rng(b).integers(0, v, 32) for b in range(bsz)]
+    prompts = [np.random.default_rng(b).integers(0, v, prompt_len) for b in range(bsz)]
     src = SyntheticSource(v, device="cuda")
     hot = HotVocab(v, src.hot_ordering()[:hot_size]) if variant == "shvs" else None
     plane = DecisionPlane(v, [SamplingParams(**vars(p)) for p in params], prompts=prompts, hot=hot)
@@ -768,6 +768,15 @@ def test_c4_full_batch_matches_oracle(torch_cuda):
     _big_batch_parity(torch_cuda, 151936, 8192, False, False, "full", 0, 32)
     import torch
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("variant", ["full", "shvs"])
+def test_c2_long_prompts_match_oracle(torch_cuda, variant):
+    """bench --config c2long: 2,048-token prompts (~2,000 penalized ids per
+    row).  The streaming kernels exclude the penalized ids from the selection
+    (pen_excl) and keep only the best penalized entries for the final merge;
+    decisions must still be the reference's (160 rows checked)."""
+    _big_batch_parity(torch_cuda, 152064, 1024, False, False, variant, 2048, 64, iters=2, prompt_len=2048)
 
 
 @pytest.mark.parametrize("raw", [False, True, "synth"])
