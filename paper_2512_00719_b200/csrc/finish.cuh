@@ -245,7 +245,7 @@ DP_DEV void warp_sort_regs(uint64_t* fkey, uint32_t* fpos) {
 // sel[0..nsel): unique (value desc, position asc) keys of the raw candidates.
 // `pp` holds the prefetched first 2*NT penalty entries.
 // Returns false when a kHot row was rejected (token left to the tail pass).
-template <typename T, int MODE, int NT, bool NUC, typename Sync>
+template <typename T, int MODE, int NT, bool NUC, bool PX, typename Sync>
 DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32_t plen, const T* rowp,
                        int64_t lo, int64_t n, const uint64_t* sel, uint32_t nsel, double sh_unpen, double mrow,
                        uint8_t* fin, const FinLayout& F, FinishScratch& fs, uint32_t t, Sync sync,
@@ -358,7 +358,7 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
   // penalized positions of this domain -> hash set (raw candidates defer to
   // them).  kHot, and long lists (a.pen_excl), streamed around the penalized
   // ids already: no hash set needed
-  const bool excl = MODE == kHot || a.pen_excl;
+  constexpr bool excl = MODE == kHot || PX;   // PX: penalized ids outside the stream (a.pen_excl)
   if (t == 0) {
     fs.nl = 0u;
     fs.np = 0u;
@@ -374,17 +374,27 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
   // penalized entries (ties at the k-th value included) can enter the ready
   // top-k, so only those are kept — a radix threshold over their exact f64
   // keys, computed on the fly from the (L2-hot) list and logits.
-  uint64_t p_thr = 0ull;
-  const bool psel = excl && plen > kPenSelCap;
-  if (psel) {
-    auto get_p = [&](uint32_t j, uint64_t& key) -> bool {
-      int32_t pos, c;
-      float x;
-      pen_entry((int32_t)j, pos, x, c);
-      if (pos < 0) return false;
-      key = f64_key(ready_penalized(x, c, p));
-      return true;
-    };
+  // rank merge (O(nsel^2 / NT) compares per thread) for short candidate lists;
+  // longer ones (long penalty lists: kp = k + |list|) take the radix cut +
+  // register sort of one warp
+#ifndef DP_RANK_MAX_ITERS
+#define DP_RANK_MAX_ITERS 48
+#endif
+  const bool fast = nsel * nsel <= (uint32_t)DP_RANK_MAX_ITERS * NT;
+  // with the penalized ids outside the stream the fast path keeps them only
+  // once the k-th unpenalized ready value rk is known: one pass, entries
+  // >= rk (late_pen); the other paths pick the k best by a radix threshold
+  const bool late_pen = PX && fast && plen > 0;
+  auto get_p = [&](uint32_t j, uint64_t& key) -> bool {
+    int32_t pos, c;
+    float x;
+    pen_entry((int32_t)j, pos, x, c);
+    if (pos < 0) return false;
+    key = f64_key(ready_penalized(x, c, p));
+    return true;
+  };
+  // the k best penalized entries' threshold key (ties at the k-th included)
+  auto pen_threshold = [&]() -> uint64_t {
     uint32_t cv = 0;
     for (int32_t j = t; j < plen; j += NT) {
       uint64_t kk;
@@ -396,20 +406,16 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
     uint32_t cnt_p = 0;
     for (int w = 0; w < NT / 32; ++w) cnt_p += fs.wc[w];
     sync();
-    p_thr = group_select_threshold<NT>(get_p, (uint32_t)plen, cnt_p, (uint32_t)k, hash, fs.wc, t, sync);
-  }
+    return group_select_threshold<NT>(get_p, (uint32_t)plen, cnt_p, (uint32_t)k, hash, fs.wc, t, sync);
+  };
+  uint64_t p_thr = 0ull;
+  const bool psel = excl && !late_pen && plen > kPenSelCap;
+  if (psel) p_thr = pen_threshold();
   const uint32_t pcap = F.cap - (uint32_t)k - 1u;   // penalized slots next to the k unpenalized ones
   // the rank-merge path keeps the penalized entries apart: ready values in
   // fcum, positions at the top of fpos (k + 2 |kept list| < lcap: no overlap)
-  // rank merge (O(nsel^2 / NT) compares per thread) for short candidate lists;
-  // longer ones (long penalty lists: kp = k + |list|) take the radix cut +
-  // register sort of one warp
-#ifndef DP_RANK_MAX_ITERS
-#define DP_RANK_MAX_ITERS 48
-#endif
-  const bool fast = nsel * nsel <= (uint32_t)DP_RANK_MAX_ITERS * NT;
   double m_sub = 0.0, m_add = 0.0;
-  for (int32_t j = t; j < plen; j += NT) {
+  for (int32_t j = t; j < plen && (!late_pen || nuc_mass); j += NT) {
     int32_t pos, c;
     float x;
     pen_entry(j, pos, x, c);
@@ -419,7 +425,7 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
         while (atomicCAS(&hash[h], 0xFFFFFFFFu, (uint32_t)pos) != 0xFFFFFFFFu) h = (h + 1u) & hmask;
       }
       const double r = ready_penalized(x, c, p);
-      if (!psel || f64_key(r) >= p_thr) {
+      if (!late_pen && (!psel || f64_key(r) >= p_thr)) {
         if (fast) {
           const uint32_t s = atomicAdd(&fs.np, 1u);
           if (s < pcap) {   // (ties at the k-th penalized value beyond kPenSelCap - k: not kept)
@@ -504,11 +510,59 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
       sync();
     }
     const uint32_t nu = min(base_u, (uint32_t)k);
-    const uint32_t np = fs.np;
     // (3) a penalized id can enter the ready top-k only if it reaches the k-th
     // unpenalized (ties kept: the merge orders them)
     const bool full_k = base_u >= (uint32_t)k;
     const double rk = full_k ? fw[k - 1] : -INFINITY;
+    if (late_pen) {
+      // keep the penalized entries >= rk; if more than fit, only the k best
+      // of them can matter (radix threshold), so keep those >= both
+      // batched: each thread issues the list loads of 4 entries, then their
+      // 4 logit gathers, so 4 entries cost two memory round trips, not 8
+      auto keep_pen = [&](uint64_t floor_key) {
+        constexpr int UB = 1;
+        for (int32_t base = (int32_t)t; base < plen; base += NT * UB) {
+          int32_t q[UB], c[UB];
+          float x[UB];
+#pragma unroll
+          for (int u = 0; u < UB; ++u) {
+            const int32_t j = base + u * NT;
+            q[u] = -1;
+            c[u] = 0;
+            if (j < plen) {
+              const int64_t qq = id_to_pos(a, pids[j]) - lo;
+              q[u] = (qq >= 0 && qq < n) ? (int32_t)qq : -1;
+              c[u] = pcnt[j];
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < UB; ++u) x[u] = q[u] >= 0 ? dom_value<T>(a, row, rowp, q[u]) : 0.f;
+#pragma unroll
+          for (int u = 0; u < UB; ++u) {
+            if (q[u] < 0) continue;
+            const double r = ready_penalized(x[u], c[u], p);
+            if (r >= rk && f64_key(r) >= floor_key) {
+              const uint32_t s2i = atomicAdd(&fs.np, 1u);
+              if (s2i < pcap) {
+                fcum[s2i] = r;
+                fpos[F.cap - 1u - s2i] = (uint32_t)q[u];
+              }
+            }
+          }
+        }
+        sync();
+      };
+      keep_pen(0ull);
+      if (fs.np > pcap) {
+        const uint64_t thr_k = pen_threshold();
+        if (t == 0) fs.np = 0u;
+        sync();
+        keep_pen(thr_k);
+      }
+      if (t == 0 && fs.np > pcap) fs.np = pcap;
+      sync();
+    }
+    const uint32_t np = fs.np;
     // (4) rank merge of U and the qualifying penalized entries P into
     // (fr, hash)[0 .. m), m = min(k, nu + |P|); order (ready desc, pos asc)
     auto before_ = [](double ra, uint32_t pa, double rb, uint32_t pb) -> bool {

@@ -137,7 +137,7 @@ DP_DEV void all_hands(const SampleArgs& a, uint8_t* smem, const PersistLayout& L
   const uint64_t tl0 = pb.tl0, tl1 = pb.tl1, tl2 = gtimer();
 #endif
   const T* rowp = reinterpret_cast<const T*>(a.logits) + (int64_t)row * a.ld;
-  finish_row<T, kFull, kPNT, false>(a, row, p, plen, rowp, 0, a.V, sel, ms.nsel, 0.0, 0.0,
+  finish_row<T, kFull, kPNT, false, false>(a, row, p, plen, rowp, 0, a.V, sel, ms.nsel, 0.0, 0.0,
                                     smem + (b ? L.cand1 : L.cand0), fin_layout(a.lcap), ms.fin, tid, sync, nullptr,
                                     0.f);
 #ifdef DP_TIMELINE
@@ -450,7 +450,7 @@ __global__ void __launch_bounds__(kPNT, 4) topk_persist_kernel(SampleArgs a) {
 #endif
       const T* rowp = reinterpret_cast<const T*>(a.logits) + (int64_t)row * a.ld;
       // the final stage's scratch lives in buffer b (its candidates are in sel now)
-      finish_row<T, kFull, kPFNT, false>(a, row, p, plen, rowp, 0, n, sel, nsel, 0.0, 0.0,
+      finish_row<T, kFull, kPFNT, false, false>(a, row, p, plen, rowp, 0, n, sel, nsel, 0.0, 0.0,
                                          reinterpret_cast<uint8_t*>(const_cast<uint4*>(cvec)), F, ms.fin, ft, sync_f,
                                          nullptr, 0.f);
       sync_f();

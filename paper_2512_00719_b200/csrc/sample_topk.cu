@@ -92,7 +92,7 @@ constexpr int kPrefetch = DP_PREFETCH;   // L2 prefetch distance, in batches
 
 // SH: TP-sharded kFull rows (a.nshard > 0), a separate instantiation so the
 // contiguous-row code keeps its single-segment stream
-template <typename T, int MODE, int NT, int U, bool NUC, bool SH>
+template <typename T, int MODE, int NT, int U, bool NUC, bool SH, bool PX = false>
 __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample_kernel(SampleArgs a) {
   constexpr int NW = NT / 32;
   constexpr int EPV = Elem<T>::kPerVec;
@@ -100,7 +100,8 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
   const int64_t n = dom_n(a, MODE);
   const int64_t lo = dom_lo(a, MODE);
   // kHot, and long penalty lists (pen_excl), stream around the penalized ids
-  const bool excl = MODE == kHot || (MODE != kHot && a.pen_excl);
+  // PX: a separate instantiation, so the plain path carries no bitmap code
+  constexpr bool excl = MODE == kHot || PX;
   const uint32_t bm_words = excl ? (uint32_t)((n + 31) / 32) + 1u : 0u;   // +1: vector window
   const TopkLayout L = topk_layout<NT>(a.wcap, a.kcap, a.lcap, (int)bm_words, a.split);
   uint64_t* cand = reinterpret_cast<uint64_t*>(smem + L.cand);
@@ -171,9 +172,17 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
   if (excl) {
     for (uint32_t i = tid; i < bm_words; i += NT) bitmap[i] = 0u;
     __syncthreads();
-    for (int32_t j = tid; j < plen; j += NT) {
-      const int64_t pos = id_to_pos(a, pids[j]) - lo;
-      if (pos >= 0 && pos < n) atomicOr(&bitmap[pos >> 5], 1u << (pos & 31));
+    // 4 list entries per thread in flight (long lists: fewer round trips)
+    for (int32_t base = tid; base < plen; base += NT * 4) {
+      int32_t pos[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int32_t j = base + u * NT;
+        pos[u] = j < plen ? (int32_t)(id_to_pos(a, pids[j]) - lo) : -1;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (pos[u] >= 0 && pos[u] < n) atomicOr(&bitmap[pos[u] >> 5], 1u << (pos[u] & 31));
     }
   }
   if (MODE == kHot) {
@@ -570,8 +579,8 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
   // ---- final stage (CTA 0): penalties, exact sort, filter, draw
   {
     const FinLayout F = fin_layout(a.lcap);
-    finish_row<T, MODE, NT, NUC>(a, row, p, plen, rowp, lo, n, sel, ms.nsel, sh_cta, mrow, smem + L.cand, F, ms.fin,
-                                 tid, [] { __syncthreads(); }, nullptr, mtau_hi);
+    finish_row<T, MODE, NT, NUC, PX>(a, row, p, plen, rowp, lo, n, sel, ms.nsel, sh_cta, mrow, smem + L.cand, F,
+                                     ms.fin, tid, [] { __syncthreads(); }, nullptr, mtau_hi);
   }
 #ifdef DP_TIMELINE
   __syncthreads();
@@ -600,7 +609,7 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
 // ---------------------------------------------------------------------------
 // host launcher
 
-template <typename T, int MODE, bool NUC, bool SH = false>
+template <typename T, int MODE, bool NUC, bool SH = false, bool PX = false>
 static cudaError_t launch_topk_t(const SampleArgs& a, int grid_rows, cudaStream_t st) {
 #ifndef DP_TOPK_NT
 #define DP_TOPK_NT 256
@@ -608,9 +617,9 @@ static cudaError_t launch_topk_t(const SampleArgs& a, int grid_rows, cudaStream_
 #endif
   constexpr int U = DP_TOPK_U, NT = DP_TOPK_NT;
   const int64_t n = MODE == kFull ? a.V : (MODE == kHot ? a.H : a.V - a.H);
-  const int bm_words = (MODE == kHot || a.pen_excl) ? (int)((n + 31) / 32) + 1 : 0;
+  const int bm_words = (MODE == kHot || PX) ? (int)((n + 31) / 32) + 1 : 0;
   const TopkLayout L = topk_layout<NT>(a.wcap, a.kcap, a.lcap, bm_words, a.split);
-  auto kern = topk_sample_kernel<T, MODE, NT, U, NUC, SH>;
+  auto kern = topk_sample_kernel<T, MODE, NT, U, NUC, SH, PX>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
@@ -631,9 +640,14 @@ static cudaError_t launch_topk_t(const SampleArgs& a, int grid_rows, cudaStream_
 template <typename T, bool NUC>
 static cudaError_t launch_topk_m(const SampleArgs& a, int mode, int grid_rows, cudaStream_t st) {
   if (mode == kFull && a.nshard > 0) return launch_topk_t<T, kFull, false, true>(a, grid_rows, st);
-  if (mode == kFull) return launch_topk_t<T, kFull, NUC>(a, grid_rows, st);
+  // long penalty lists (a.pen_excl): the instantiation that streams around
+  // the penalized ids
+  if (mode == kFull)
+    return a.pen_excl ? launch_topk_t<T, kFull, NUC, false, true>(a, grid_rows, st)
+                      : launch_topk_t<T, kFull, NUC>(a, grid_rows, st);
   if (mode == kHot) return launch_topk_t<T, kHot, NUC>(a, grid_rows, st);
-  return launch_topk_t<T, kTail, NUC>(a, grid_rows, st);
+  return a.pen_excl ? launch_topk_t<T, kTail, NUC, false, true>(a, grid_rows, st)
+                    : launch_topk_t<T, kTail, NUC>(a, grid_rows, st);
 }
 
 // dynamic shared memory of a top-k launch with the call's capacities

@@ -27,7 +27,7 @@ ap.add_argument("--grow", type=int, default=0, help="decide (and record) this ma
 args = ap.parse_args()
 cfg = bench.CONFIGS[args.config]
 v, b = cfg["V"], cfg["B"]
-prompts = [np.random.default_rng(s).integers(0, v, 32) for s in range(b)]
+prompts = [np.random.default_rng(s).integers(0, v, cfg.get("prompt_len", 32)) for s in range(b)]
 src = SyntheticSource(v, device="cuda")
 hot = HotVocab(v, src.hot_ordering()[: args.hot]) if args.variant == "shvs" else None
 plane = DecisionPlane(v, [bench.row_params(cfg, s) for s in range(b)], prompts=prompts, hot=hot,
