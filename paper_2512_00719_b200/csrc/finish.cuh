@@ -367,6 +367,7 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
   if (!excl)
     for (uint32_t i = t; i < hcap; i += NT) hash[i] = 0xFFFFFFFFu;
   sync();
+  lap(8);
   const bool nuc_mass = nuc && MODE != kHot;
   const float s2 = (float)(1.4426950408889634 / p.temperature);
   const double cref_r = (double)cref / p.temperature;   // cref in ready units
@@ -484,6 +485,7 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
       fkey[rank] = key;
     }
     sync();
+    lap(9);
     // (2) the k largest unpenalized, in order: their ready values keep the raw
     // order (x / tau is monotone), so a prefix count over the sorted keys ranks
     // them; list U -> (fw, fpos)[0 .. nu)
@@ -510,6 +512,7 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
       sync();
     }
     const uint32_t nu = min(base_u, (uint32_t)k);
+    lap(10);
     // (3) a penalized id can enter the ready top-k only if it reaches the k-th
     // unpenalized (ties kept: the merge orders them)
     const bool full_k = base_u >= (uint32_t)k;
@@ -520,7 +523,7 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
       // batched: each thread issues the list loads of 4 entries, then their
       // 4 logit gathers, so 4 entries cost two memory round trips, not 8
       auto keep_pen = [&](uint64_t floor_key) {
-        constexpr int UB = 1;
+        constexpr int UB = 4;
         for (int32_t base = (int32_t)t; base < plen; base += NT * UB) {
           int32_t q[UB], c[UB];
           float x[UB];
@@ -563,6 +566,7 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
       sync();
     }
     const uint32_t np = fs.np;
+    lap(11);
     // (4) rank merge of U and the qualifying penalized entries P into
     // (fr, hash)[0 .. m), m = min(k, nu + |P|); order (ready desc, pos asc)
     auto before_ = [](double ra, uint32_t pa, double rb, uint32_t pb) -> bool {

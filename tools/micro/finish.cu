@@ -122,7 +122,9 @@ int main(int argc, char** argv) {
       if (e != cudaSuccess) { printf("err %s\n", cudaGetErrorString(e)); return 1; }
     }
     int tk; cudaMemcpy(&tk, tok, 4, cudaMemcpyDeviceToHost);
-    printf("  laps/row: 12 %lld 13 %lld 14 %lld 16 %lld 15 %lld 21(2nd draw) %lld\n", st[12] / (8 * nblk), st[13] / (8 * nblk), st[14] / (8 * nblk), st[16] / (8 * nblk), st[15] / (8 * nblk), st[21] / (8 * nblk));
+    printf("  laps/row:");
+    for (int sl : {8, 12, 9, 10, 11, 13, 14, 16, 15}) printf(" %d:%lld", sl, st[sl] / (8 * nblk));
+    printf("\n");
     for (int i = 0; i < 24; ++i) st[i] = 0;
     printf("[%d CTAs] finish_row minBlocks=%d: %lld cycles (token %d); draw in loop %lld, draw once %lld, draw interleaved with finish_row %lld, draw COLD %lld\n", nblk, mb, cyc[0], tk, cyc[1], cyc[2], cyc[5], cyc[6]);
   }
