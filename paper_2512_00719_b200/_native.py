@@ -133,6 +133,12 @@ def load(path: str = LIB_PATH) -> C.CDLL:
             raise NativeUnavailable(
                 f"{path} is missing: build it with `python build.py` (nvcc, sm_100a). "
                 "There is no CPU fallback for the decision plane.")
+        # torch first: its libnccl.so.2 (DT_NEEDED of libtorch_cuda) must be the
+        # process's copy before the library resolves NCCL (collective.cu reuses
+        # an already-loaded libnccl.so.2; loading the system one first would
+        # break a later `import torch` with a different NCCL version)
+        import torch  # noqa: F401
+
         lib = C.CDLL(path)
         for name, (args, res) in _SIGS.items():
             fn = getattr(lib, name)

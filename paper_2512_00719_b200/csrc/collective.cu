@@ -7,7 +7,10 @@
 // collective).  NCCL is resolved at run time with dlopen: inside a PyTorch
 // process the libnccl.so.2 torch already loaded is reused (RTLD_NOLOAD), so
 // the library never drags a second NCCL into the process; elsewhere the
-// system libnccl.so.2 is opened.  Nothing here links NCCL at build time.
+// system libnccl.so.2 is opened.  (A process that will import torch must do
+// so before the first collective call — _native.load() imports torch first —
+// or the system copy would shadow torch's.)  Nothing here links NCCL at
+// build time.
 #include <dlfcn.h>
 
 #include <cstdio>

@@ -180,3 +180,48 @@ def test_collective_entry_points_resolve_nccl(lib):
     assert any(bytes(uid))
     assert lib.dp_allgather_tokens(None, None, 4, None, None) == N.DP_ERR_ARG
     assert lib.dp_allgather_tokens(None, None, 0, C.c_void_p(1), None) == N.DP_OK
+
+
+def test_hot_size_controller_boundary_logic_on_cpu():
+    """control.HotSizeController's host logic (service.py:602-610 apply_control
+    + run_iteration): a requested size is validated now and applied only at the
+    next iteration boundary; the acceptance window averages the observed
+    calls.  A stand-in plane (no kernels) carries the hot set."""
+    import torch
+
+    from paper_2512_00719_b200.control import HotSizeController
+    from paper_2512_00719_b200.shvs import HotVocab
+
+    class Plane:
+        vocab_size, batch = 64, 4
+
+        def __init__(self):
+            self.hot = None
+
+        def set_hot(self, hot):
+            self.hot = hot
+
+    class D:
+        def __init__(self, flags):
+            self.flags = torch.tensor(flags, dtype=torch.uint8)
+
+    plane = Plane()
+    master = HotVocab(64, np.arange(64)[::-1].copy())
+    ctl = HotSizeController(plane, master, grid=(8, 16, 32), window=8)
+    with pytest.raises(ValueError):
+        ctl.request(0)
+    with pytest.raises(ValueError):
+        ctl.request(65)
+    with pytest.raises(ValueError):
+        ctl.begin_iteration(0)          # no hot set yet
+    ctl.request(16)
+    assert plane.hot is None            # parked until the boundary
+    hot = ctl.begin_iteration(3)
+    assert hot.size == 16 and list(hot.hot_ids) == list(master.hot_ids[:16]) and ctl.history == [(3, 16)]
+    assert ctl.begin_iteration(4) is hot and ctl.history == [(3, 16)]
+    for fl in ([2, 0, 2, 2], [0, 0, 2, 0], [2, 2, 2, 2]):
+        ctl.end_iteration(0, D(fl))     # no logits: observe only
+    # window of 8 decisions = the last two calls
+    assert abs(ctl.acceptance_rate() - 5 / 8) < 1e-12
+    with pytest.raises(ValueError):
+        ctl.refit(None)                 # no cost model yet
