@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(kPNT, 4) topk_persist_kernel(SampleArgs a) {
 #pragma unroll
             for (int e = 0; e < EPV; ++e) mx = fmaxf(mx, vec_elem<T>(v[q], e));
           const uint32_t kw = (kp + kPSW - 1) / kPSW;
-          int rw = (int)ceilf(kEstOver * (float)kp * (float)(32 * U * EPV) / (float)max((int64_t)1, n));
+          int rw = (int)ceilf(est_over(kp, false) * (float)kp * (float)(32 * U * EPV) / (float)max((int64_t)1, n));
           rw = max(1, min(32, rw));
           const uint32_t sorted = warp_sort_desc(f32_key(mx));
           const uint32_t t_lbk = __shfl_sync(0xffffffffu, sorted, kw <= 32 ? kw - 1 : 31);

@@ -359,7 +359,7 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
       }
       const uint32_t kw = (kp + NW - 1) / NW;
       const float seg = (float)max((int64_t)1, seg_elems);
-      int rw = (int)ceilf(kEstOver * (float)kp * (float)(32 * U * EPV) / seg);
+      int rw = (int)ceilf(est_over(kp, nuc) * (float)kp * (float)(32 * U * EPV) / seg);
       rw = max(1, min(32, rw));
       const uint32_t sorted = warp_sort_desc(f32_key(mx));
       const uint32_t t_lbk = __shfl_sync(0xffffffffu, sorted, kw <= 32 ? kw - 1 : 31);

@@ -9,13 +9,16 @@ namespace dp {
 
 enum Mode : int { kFull = 0, kHot = 1, kTail = 2 };
 // Admission threshold estimate of the streaming top-k kernels: the first
-// batch's sample estimates the (kEstOver * kp)-th largest of the segment.  A
-// too-high estimate (fewer than kp admitted) costs a whole re-stream, which
-// long penalty lists (kp = k + |list| ~ 200) made frequent at 2x.
-#ifndef DP_EST_OVER
-#define DP_EST_OVER 4.0f
-#endif
-constexpr float kEstOver = DP_EST_OVER;
+// batch's sample estimates the (est * kp)-th largest of the segment.  A
+// too-high estimate (fewer than kp admitted) costs a whole re-stream of the
+// row, which the C2 distribution hits at est = 2 (1,000 steps: 150 vs 131 us
+// at est = 4); every extra admission costs select work, which nucleus rows
+// (kp >= 256) pay for at est = 4 (C5 full path 2.42 vs 2.75 ms;
+// profiles/r2/est_over_ab.txt).
+DP_DEV float est_over(uint32_t kp, bool nucleus) {
+  (void)kp;
+  return nucleus ? 2.0f : 4.0f;
+}
 constexpr int kHotSortMax = 4096;   // SHVS hot prefixes up to this size take K1h (sample_hot.cu)
 constexpr int kMaxShards = 8;
 

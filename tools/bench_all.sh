@@ -11,4 +11,5 @@ run c3 --config c3 --steps 300 --warmup 5 --no-cpu-baseline
 run c5 --config c5 --steps 50 --warmup 3 --no-cpu-baseline
 run c5_full --config c5 --variant full --steps 30 --warmup 3 --no-cpu-baseline --no-shvs
 run c4 --config c4 --steps 50 --warmup 3 --no-cpu-baseline
+run c2long --config c2long --steps 100 --warmup 5 --no-cpu-baseline
 run ref --impl reference --steps 5 --warmup 3
