@@ -422,6 +422,7 @@ def measure_shvs_e2e(args, cfg, plane_kw, src, seq_ids, dev, shard, world):
 
     v = cfg["V"]
     plane = DecisionPlane(v, **plane_kw)
+    plane.plan_flags = args.plan_flags
     tdt = torch.float32 if cfg["dtype"] == "f32" else torch.bfloat16
     h, sizing_info = shvs_hot_size(args, plane, src, seq_ids, dev, tdt)
     esz = 4 if cfg["dtype"] == "f32" else 2
@@ -555,6 +556,7 @@ def run_ours(args, cfg):
     hot = None
     plane = DecisionPlane(v, params, prompts=prompts, seq_ids=seq_ids, hot=hot, device=dev,
                           max_generated=RESET_EVERY + 8, split=args.split, kernel=args.kernel)
+    plane.plan_flags = args.plan_flags
     tdt = torch.float32 if cfg["dtype"] == "f32" else torch.bfloat16
     sizing_info = None
     if variant == "shvs":
@@ -779,6 +781,7 @@ def main():
     ap.add_argument("--variant", default=None, choices=["full", "shvs"],
                     help="default: full (C5: shvs, the config's SHVS mix)")
     ap.add_argument("--split", type=int, default=0)
+    ap.add_argument("--plan-flags", type=int, default=0, help="extra DP_PLAN_* bits for every plane (A-B)")
     ap.add_argument("--kernel", type=int, default=0, help="dp_plan_t.kernel: 0 auto, 1 CTA/cluster, 2 warp-per-row")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-seconds", type=float, default=5.0)

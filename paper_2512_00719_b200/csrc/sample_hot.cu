@@ -12,12 +12,16 @@
 // the first min(k, H) entries (all H with top-k off).  No estimate, no
 // re-stream, no fallback: nucleus rows (top-p / min-p without top-k), which
 // K1 decides through a 256-entry list plus a general-kernel fallback, are
-// exact here too.  Opt-in (DP_PLAN_HOT_SORT: nucleus rows, route_row
-// use_hot_sort 1; DP_PLAN_HOT_SORT_ALL: every row, 2): the streaming kernels
-// stay faster at the bench shapes — C2 top-k rows 36 vs ~70 us, C5 nucleus
-// rows 1,037 vs 1,234 us per step at H = 2,048 (the 66-stage shared-memory
-// sort of every row is the cost; profiles/r2/k1h).  One CTA per row
-// (grid-stride over rows); with H = 2,048 a CTA holds 42 KB.
+// exact here too.  Nucleus rows skip the full sort in the common case: the
+// top-224 by a block radix select (digits from the keys' highest differing
+// bit), one warp sorts them, and warp_filter_draw_nuc decides against the
+// exact f64 mass of the whole hot set; the full sort runs only when the kept
+// set (or a neutral row's draw) leaves that list.  Opt-in (DP_PLAN_HOT_SORT:
+// nucleus rows, route_row use_hot_sort 1; DP_PLAN_HOT_SORT_ALL: every row,
+// 2): the streaming kernels stay faster at the bench shapes — C2 top-k rows
+// 36 vs ~70 us, C5 nucleus rows 1,045 vs 1,306 us per step at H = 2,048
+// (per row, two f64 exps and an f64 divide per hot value dominate;
+// profiles/r2/k1h).  One CTA per row (grid-stride over rows).
 #include "sampler.cuh"
 #include "select.cuh"
 #include "finish.cuh"
@@ -26,6 +30,8 @@ namespace dp {
 
 constexpr int kHSNT = 256;          // threads per CTA
 constexpr int kHSW = kHSNT / 32;
+constexpr int kHSCumMin = 1152;     // doubles: the nucleus path's scratch (2 KB keys + 1 KB pos + 3 x 256 doubles)
+constexpr int kHSNucM = 224;        // nucleus rows: the M largest are selected first (ties may add up to 256)
 
 DP_DEV double key_f64(uint64_t k) {
   const uint64_t b = (k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k;
@@ -74,9 +80,10 @@ DP_DEV uint32_t hs_count(bool pred, uint32_t* cnt, uint32_t* bcu) {
 template <typename T>
 __global__ void __launch_bounds__(kHSNT) hot_sort_kernel(SampleArgs a, int hp) {
   extern __shared__ __align__(16) uint8_t smem[];
-  uint64_t* key = reinterpret_cast<uint64_t*>(smem);   // [hp] ready keys; after the sort: ready values
-  double* cum = reinterpret_cast<double*>(key + hp);    // [hp] prefix masses
-  uint32_t* pos = reinterpret_cast<uint32_t*>(cum + hp);   // [hp] hot positions
+  const int ccap_d = hp > kHSCumMin ? hp : kHSCumMin;   // prefix masses / nucleus scratch (doubles)
+  uint64_t* key = reinterpret_cast<uint64_t*>(smem);   // [hp] ready keys
+  double* cum = reinterpret_cast<double*>(key + hp);    // [ccap_d] prefix masses
+  uint32_t* pos = reinterpret_cast<uint32_t*>(cum + ccap_d);   // [hp] hot positions
   __shared__ HotSortShared S;
   const uint32_t tid = threadIdx.x, lane = tid & 31u;
   const int64_t H = a.H;
@@ -152,7 +159,7 @@ __global__ void __launch_bounds__(kHSNT) hot_sort_kernel(SampleArgs a, int hp) {
       // top-k rows: radix threshold of the k-th largest key (ties at it
       // included), the >= k survivors compacted and ordered by one warp
       auto get_k = [&](uint32_t i, uint64_t& kk) -> bool { kk = key[i]; return true; };
-      uint32_t* hist = reinterpret_cast<uint32_t*>(pos + hp) ;   // 256 u32 past the arrays (smem sized for it)
+      uint32_t* hist = reinterpret_cast<uint32_t*>(pos + hp);   // 256 u32 past the arrays (smem sized for it)
       const uint64_t t = group_select_threshold<kHSNT>(get_k, (uint32_t)H, (uint32_t)H, (uint32_t)n, hist, S.bcu,
                                                        tid, [] { __syncthreads(); });
       uint64_t* ck = reinterpret_cast<uint64_t*>(cum);          // survivors (scratch in the prefix array)
@@ -181,6 +188,132 @@ __global__ void __launch_bounds__(kHSNT) hot_sort_kernel(SampleArgs a, int hp) {
         }
         __syncthreads();
         sorted = true;
+      }
+    }
+    if (!sorted && n == (int)H && H > 256) {
+      // nucleus rows (top-k off): the top-M by a block radix select (digits
+      // start at the keys' highest differing bit, so the histogram spreads),
+      // one warp sorts them, and warp_filter_draw_nuc decides against the
+      // exact mass of the whole hot set — the full sort only when the kept
+      // set (or, for neutral rows, the draw) leaves the M (fallback)
+      uint32_t* hist = reinterpret_cast<uint32_t*>(pos + hp);
+      uint64_t* ck = reinterpret_cast<uint64_t*>(cum);      // [256] survivors
+      uint32_t* cpos = reinterpret_cast<uint32_t*>(ck + 256);   // [256]
+      double* fr = reinterpret_cast<double*>(cpos + 256);    // [256] sorted ready values
+      double* fw = fr + 256;
+      double* fc = fw + 256;
+      // kmax / kmin of the keys of the hot set, and r0 / the mass relative to it
+      uint64_t kmx = 0ull, kmn = ~0ull;
+      for (int i = (int)tid; i < (int)H; i += kHSNT) {
+        kmx = key[i] > kmx ? key[i] : kmx;
+        kmn = key[i] < kmn ? key[i] : kmn;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t a1 = __shfl_xor_sync(0xffffffffu, kmx, o), b1 = __shfl_xor_sync(0xffffffffu, kmn, o);
+        kmx = a1 > kmx ? a1 : kmx;
+        kmn = b1 < kmn ? b1 : kmn;
+      }
+      __shared__ uint64_t s_mx[kHSW], s_mn[kHSW];
+      if (lane == 0) {
+        s_mx[tid >> 5] = kmx;
+        s_mn[tid >> 5] = kmn;
+      }
+      __syncthreads();
+      kmx = s_mx[0];
+      kmn = s_mn[0];
+      for (int w = 1; w < kHSW; ++w) {
+        kmx = s_mx[w] > kmx ? s_mx[w] : kmx;
+        kmn = s_mn[w] < kmn ? s_mn[w] : kmn;
+      }
+      const double rtop = key_f64(kmx);
+      double tw = 0.0;
+      for (int i = (int)tid; i < (int)H; i += kHSNT) tw += exp(key_f64(key[i]) - rtop);
+      const double total_w = hs_sum(tw, S.red, S.bc);   // hot-set mass relative to the top value
+      // threshold t: >= M keys are >= t (ties at it included)
+      uint64_t t = kmn;
+      if (kmx != kmn) {
+        const int hb = 63 - __clzll((long long)(kmx ^ kmn));
+        uint64_t prefix = kmx & ~((hb == 63) ? 0ull : ((2ull << hb) - 1ull));
+        uint32_t need = (uint32_t)kHSNucM;
+        for (int hi = hb;; hi -= 8) {
+          const int lo = hi >= 7 ? hi - 7 : 0;
+          const uint64_t hmask = (hi == 63) ? ~0ull : ((2ull << hi) - 1ull);   // bits <= hi
+          for (int i = (int)tid; i < 256; i += kHSNT) hist[i] = 0u;
+          __syncthreads();
+          for (int i = (int)tid; i < (int)H; i += kHSNT) {
+            const uint64_t kk = key[i];
+            if ((kk & ~hmask) == prefix) atomicAdd(&hist[(uint32_t)((kk & hmask) >> lo)], 1u);
+          }
+          __syncthreads();
+          if (tid < 32) {
+            const DigitHit h = warp_find_digit(hist, need);
+            if (tid == 0) {
+              S.bcu[0] = h.digit;
+              S.bcu[1] = h.above;
+              S.bcu[2] = h.inbin;
+            }
+          }
+          __syncthreads();
+          prefix |= (uint64_t)S.bcu[0] << lo;
+          need -= S.bcu[1];
+          const bool done = S.bcu[2] == need || lo == 0;
+          __syncthreads();
+          if (done) break;
+        }
+        t = prefix;
+      }
+      if (tid == 0) S.bcu[3] = 0u;
+      __syncthreads();
+      for (int i = (int)tid; i < (int)H; i += kHSNT) {
+        const uint64_t kk = key[i];
+        if (kk >= t) {
+          const uint32_t o = atomicAdd(&S.bcu[3], 1u);
+          if (o < 256u) {
+            ck[o] = kk;
+            cpos[o] = pos[i];
+          }
+        }
+      }
+      __syncthreads();
+      const uint32_t c = S.bcu[3];
+      if (c <= 256u) {
+        if (tid < 32) {
+          warp_topk_sort(ck, cpos, c, c, hist);   // c > 64: sort only (no cut)
+          for (uint32_t j = lane; j < c; j += 32) fr[j] = key_f64(ck[j]);
+          __syncwarp();
+          bool fb = false;
+          const DrawResult d = warp_filter_draw_nuc(fr, (int32_t)c, knobs_of(p), u[0], total_w, fw, fc, fb);
+          if (lane == 0) S.bcu[2] = fb ? 1u : 0u;
+          if (!fb) {
+            double margin = d.margin;
+            if (!tail_empty && !deferred) margin = fmin(margin, fabs(u[1] - alpha));
+            const int32_t tok = pos_to_id(a, (int64_t)cpos[d.index]);
+            if (lane == 0) {
+              a.token[row] = tok;
+              a.logprob[row] = d.logprob;
+              uint8_t fl = DP_FLAG_ACCEPTED_HOT;
+              if (margin < kBoundaryEps) fl |= DP_FLAG_NEAR_BOUNDARY;
+              a.flags[row] = fl;
+              if (a.dbg.margin) a.dbg.margin[row] = margin;
+              if (a.dbg.kept) a.dbg.kept[row] = d.kept;
+              if (a.dbg.alpha) a.dbg.alpha[row] = alpha;
+              if (deferred) push_resum(a, row, sH);   // the exact re-sum decides, then records
+            }
+            if (!deferred) warp_record_token(a, row, tok);   // fused K5
+            if (a.dbg.topk_ids) {
+              const int m = min((int)c, a.dbg.topk_stride);
+              for (int j = (int)lane; j < m; j += 32) {
+                a.dbg.topk_ids[(int64_t)row * a.dbg.topk_stride + j] = pos_to_id(a, (int64_t)cpos[j]);
+                if (a.dbg.topk_ready) a.dbg.topk_ready[(int64_t)row * a.dbg.topk_stride + j] = fr[j];
+              }
+            }
+          }
+        }
+        __syncthreads();
+        const bool fb_all = S.bcu[2] != 0u;
+        __syncthreads();
+        if (!fb_all) continue;   // decided
       }
     }
     if (!sorted) {
@@ -310,7 +443,8 @@ __global__ void __launch_bounds__(kHSNT) hot_sort_kernel(SampleArgs a, int hp) {
 size_t hot_sort_smem(int64_t H) {
   int hp = 512;   // the top-k scratch (256 keys + positions) lives in the prefix array
   while (hp < H) hp <<= 1;
-  return (size_t)hp * 20u + 1024u;   // + the radix histogram
+  const int cd = hp > kHSCumMin ? hp : kHSCumMin;
+  return (size_t)hp * 12u + (size_t)cd * 8u + 1024u;   // keys + positions, prefix masses, radix histogram
 }
 
 cudaError_t launch_hot_sort(const SampleArgs& a, int dtype, cudaStream_t st) {

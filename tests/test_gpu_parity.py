@@ -706,7 +706,8 @@ def _bench_params(cfg_mix, b):
     return O.Params(**kw, seed=0)
 
 
-def _big_batch_parity(torch, v, bsz, bf16, mix, variant, hot_size, check_every, iters=2, raw=True, prompt_len=32):
+def _big_batch_parity(torch, v, bsz, bf16, mix, variant, hot_size, check_every, iters=2, raw=True, prompt_len=32,
+                      plan_flags=0):
     from paper_2512_00719_b200 import DecisionPlane, HotVocab, SamplingParams
     from paper_2512_00719_b200.synthetic import SyntheticSource
 
@@ -715,6 +716,7 @@ def _big_batch_parity(torch, v, bsz, bf16, mix, variant, hot_size, check_every, 
     src = SyntheticSource(v, device="cuda")
     hot = HotVocab(v, src.hot_ordering()[:hot_size]) if variant == "shvs" else None
     plane = DecisionPlane(v, [SamplingParams(**vars(p)) for p in params], prompts=prompts, hot=hot)
+    plane.plan_flags = plan_flags
     check = list(range(0, bsz, check_every))
     states = {b: O.State.new(prompts[b], v) for b in check}
     tail = O.tail_ids_of(hot.hot_ids, v) if hot is not None else None
@@ -791,6 +793,17 @@ def test_c5_mix_shvs_with_producer_fused_summary(torch_cuda):
     """C5 row mix (bf16, 5 kinds, penalties alternating) at V=152,064, SHVS
     with the summary the producer emits while writing the bf16 rows."""
     _big_batch_parity(torch_cuda, 152064, 2048, True, True, "shvs", 4096, 8, raw="synth")
+
+
+@pytest.mark.parametrize("hot_size", [512, 2048])
+def test_c5_mix_shvs_with_exact_sort_hot_pass(torch_cuda, hot_size):
+    """C5 row mix (bf16) with the hot pass's nucleus rows decided by K1h
+    (DP_PLAN_HOT_SORT: top-224 select + sort, exact hot-set mass, full sort on
+    fallback); 256 rows checked against the oracle."""
+    from paper_2512_00719_b200 import _native as N
+
+    _big_batch_parity(torch_cuda, 152064, 2048, True, True, "shvs", hot_size, 8, raw="synth",
+                      plan_flags=N.PLAN_HOT_SORT)
 
 
 @pytest.mark.parametrize("bf16", [False, True])

@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--kernel", type=int, default=0)
     ap.add_argument("--hot", type=int, default=4096)
     ap.add_argument("--bf16", action="store_true")
+    ap.add_argument("--plan-flags", type=int, default=0)
     ap.add_argument("--extra", default="", help="comma list: fused (producer-fused summary), curve (K6), "
                                                 "summary (K2 penalized)")
     args = ap.parse_args()
@@ -39,6 +40,7 @@ def main():
     params = [bench.row_params(cfg, s) for s in range(b)]
     plane = DecisionPlane(v, params, prompts=prompts, hot=hot, split=args.split, kernel=args.kernel,
                           max_generated=136)
+    plane.plan_flags = args.plan_flags
     perm = hot.device_maps(plane.device)[0] if hot is not None else None
     dt = torch.bfloat16 if (args.bf16 or cfg["dtype"] == "bf16") else torch.float32
     extra = set(filter(None, args.extra.split(",")))
