@@ -42,7 +42,7 @@ namespace dp {
 constexpr int kWXcap = 512;   // candidate keys per warp buffer (>= kWarpKpMax + one batch of admissions)
 constexpr int kWHcap = 512;   // penalty hash slots (>= 2 * kWarpPenCap)
 constexpr int kMW = 4;        // warps per row (one CTA per row)
-constexpr int kWU = 8;        // 16-byte vectors in flight per lane
+constexpr int kWU = 4;        // 16-byte vectors in flight per lane
 constexpr int kMWBlocks = 7;
 constexpr int kWQcap = 256;   // admitted-vector queue per warp (>= 32 lanes * kWU)
 constexpr int kFLcap = 320;   // final list (k <= 64 cut keys + <= 256 penalized), in the queue area  // resident CTAs per SM the register budget targets (1,024 rows in one wave)
@@ -171,6 +171,7 @@ __global__ void __launch_bounds__(kMW * 32, kMWBlocks) warp_sample_kernel(Sample
     // penalty list ids -> absolute row positions, fetched while the first
     // batch is in flight (consumed after the stream; kWarpPenCap = 2 * 128)
     int32_t pa_r[2] = {-1, -1}, pc_r[2] = {0, 0};
+    float px_r[2] = {0.f, 0.f};   // their raw logits, gathered during the stream too
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
       const int32_t j = (int32_t)threadIdx.x + i * kMW * 32;
@@ -179,6 +180,9 @@ __global__ void __launch_bounds__(kMW * 32, kMWBlocks) warp_sample_kernel(Sample
         pc_r[i] = pcnt[j];
       }
     }
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+      if (pa_r[i] >= 0) px_r[i] = row_value<T>(a, row, pa_r[i]);
 
     // ---- threshold from the strided first batch: each lane keeps its top-2
     // sample values; warp w takes the ceil(kp/4)-th largest of its 64 kept
@@ -403,7 +407,7 @@ __global__ void __launch_bounds__(kMW * 32, kMWBlocks) warp_sample_kernel(Sample
         const int64_t pa = pa_r[i];   // absolute row position
         const int64_t q = pa - lo;
         const bool in = q >= 0 && q < n;
-        const float x = row_value<T>(a, row, pa);
+        const float x = px_r[i];
         const double r = ready_penalized(x, pc_r[i], p);
         S.pq[j] = in ? (int32_t)q : -1;
         S.pkey[j] = f64_key(r);
