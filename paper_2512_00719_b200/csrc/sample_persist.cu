@@ -175,6 +175,9 @@ __global__ void __launch_bounds__(kPNT, 4) topk_persist_kernel(SampleArgs a) {
   auto cvec_of = [&](int b) { return reinterpret_cast<uint4*>(smem + (b ? L.cand1 : L.cand0)); };
   auto cidx_of = [&](int b) { return reinterpret_cast<int32_t*>(cvec_of(b) + ccap); };
 
+  // the CTA's last top-k row, finished by all 8 warps at ONE call site after
+  // both role loops (every warp then executes the same barrier instructions)
+  int ah_row = -1, ah_b = 0;
   if (tid < (uint32_t)kPSNT) {
     // ======================= streaming warps =======================
     const uint32_t warp = tid >> 5, lane = tid & 31u;
@@ -388,9 +391,10 @@ __global__ void __launch_bounds__(kPNT, 4) topk_persist_kernel(SampleArgs a) {
 #endif
       }
       sync_s();
-      if (!more_topk_rows(a, ridx)) {   // the CTA's last row: every warp finishes it
-        all_hands<T>(a, smem, L, ms, b, row, p, plen, kp);
-        return;
+      if (!more_topk_rows(a, ridx)) {   // the CTA's last row: every warp finishes it (below)
+        ah_row = row;
+        ah_b = b;
+        break;
       }
       if (tid == 0) mbar_arrive(&ms.full[b]);   // release: the buffer and its description
       ++j;
@@ -411,9 +415,10 @@ __global__ void __launch_bounds__(kPNT, 4) topk_persist_kernel(SampleArgs a) {
       if (route_row(a, kFull, k, plen, n) != kRouteTopk) continue;
       const uint32_t kp = (uint32_t)min64(n, (int64_t)k + plen);
       const int b = (int)(j & 1u);
-      if (!more_topk_rows(a, ridx)) {   // the last row: joined by the streaming warps
-        all_hands<T>(a, smem, L, ms, b, row, p, plen, kp);
-        return;
+      if (!more_topk_rows(a, ridx)) {   // the last row: joined by the streaming warps (below)
+        ah_row = row;
+        ah_b = b;
+        break;
       }
       mbar_wait(&ms.full[b], (j >> 1) & 1u);
       PBuf& pb = ms.buf[b];
@@ -466,6 +471,12 @@ __global__ void __launch_bounds__(kPNT, 4) topk_persist_kernel(SampleArgs a) {
 #endif
       ++j;
     }
+  }
+  if (ah_row >= 0) {
+    const dp_params_t p = a.params[ah_row];
+    const int32_t plen = pen_len(a, ah_row, p);
+    const uint32_t kp = (uint32_t)min64(n, (int64_t)p.top_k + plen);
+    all_hands<T>(a, smem, L, ms, ah_b, ah_row, p, plen, kp);
   }
 }
 

@@ -48,5 +48,31 @@ for bt, t in ((12, 4), (160, 8)):
     for it in range(2):
         plane_t.sample_sharded([xt[:, s * w:(s + 1) * w].contiguous() for s in range(t)], it)
         assert plane_t.last_stitched is False
+# round 2: K1p (persistent, warp-specialised; forced on a small batch so the
+# grid loops), K1h (exact-sort hot pass, every row / nucleus rows), long
+# penalty lists (pen_excl instantiation + late penalized keep), the
+# producer-fused summary (8-CTA clusters) and the bytes-touched counters
+from paper_2512_00719_b200 import _native as N  # noqa: E402
+
+bp = 700
+pp = [SamplingParams(**kinds[0 if i % 3 else 3], seed=i) for i in range(bp)]
+prp = [np.random.default_rng(i).integers(0, v, 24) for i in range(bp)]
+plane_p = DecisionPlane(v, pp, prompts=prp, max_generated=16)
+plane_p.plan_flags = N.PLAN_FORCE_PERSIST
+plane_p._plan.flags = N.PLAN_FORCE_PERSIST
+xp = src.generate(1, range(bp))
+for it in range(2):
+    plane_p.sample(xp, it, debug=(it == 1))
+for flags in (N.PLAN_HOT_SORT_ALL, N.PLAN_HOT_SORT):
+    plane_h = DecisionPlane(v, params, prompts=prompts, hot=hot, max_generated=16)
+    plane_h.plan_flags = flags
+    plane_h.sample(xs, 4, variant="shvs", summary=summ, summary_raw=True, debug=True)
+long_prompts = [np.random.default_rng(i).integers(0, v, 600) for i in range(b)]
+plane_l = DecisionPlane(v, params, prompts=long_prompts, hot=hot, max_generated=16)
+for it in range(2):
+    plane_l.sample(x, it)
+    plane_l.sample(xs, 20 + it, variant="shvs", summary=summ, summary_raw=True)
+xf, sf = src.generate(2, range(b), perm=hot.device_maps(plane_s.device)[0], summary_params=plane_s.params_dev)
+plane_s.sample(xf, 30, variant="shvs", summary=sf, summary_raw=True)
 torch.cuda.synchronize()
 print("sanitize workload done")
