@@ -11,12 +11,12 @@
 // (row = blockIdx.x + i * gridDim.x).  Its warps split into two roles joined
 // by two double-buffered candidate buffers in shared memory and four
 // mbarriers (full[2] / empty[2]):
-//   * 6 streaming warps: threshold from the first register batch, 16-byte
+//   * 5 streaming warps: threshold from the first register batch, 16-byte
 //     streaming loads, vector admission into candidate buffer i & 1, the
 //     overflow / re-stream rule — exactly K1's stream stage — then hand the
 //     buffer over and start the next row at once;
-//   * 2 finishing warps: exact radix select of the raw top-(k + |list|)
-//     (select.cuh), release the buffer, then finish_row (finish.cuh) on 64
+//   * 3 finishing warps: exact radix select of the raw top-(k + |list|)
+//     (select.cuh), release the buffer, then finish_row (finish.cuh) on 96
 //     threads — penalties in IEEE f64, /tau, canonical order, top-p / min-p,
 //     inverse-CDF draw, fused penalty-state update — while the streaming
 //     warps already stream the next row.
@@ -29,9 +29,15 @@
 namespace dp {
 
 constexpr int kPNT = 256;            // threads per CTA
-constexpr int kPSW = 6;              // streaming warps
+#ifndef DP_PERSIST_SW
+#define DP_PERSIST_SW 5
+#endif
+// 5 streaming + 3 finishing warps: C2 122 us vs 129 (6 + 2), 145 (7 + 1),
+// 132 (3 + 5); 4 + 4 is faster on fresh lists (120) but 140 us once the
+// penalty lists grow (profiles/r2/k1p/warp_split_ab.txt)
+constexpr int kPSW = DP_PERSIST_SW;  // streaming warps
 constexpr int kPSNT = kPSW * 32;     // 192
-constexpr int kPFNT = kPNT - kPSNT;  // 64 finishing threads
+constexpr int kPFNT = kPNT - kPSNT;  // finishing threads
 constexpr uint32_t kBarStream = 1, kBarFin = 2;   // named barriers (0 = __syncthreads)
 #ifndef DP_PERSIST_U_BF16
 #define DP_PERSIST_U_BF16 4
