@@ -310,7 +310,16 @@ int dp_sample_full(const void* logits, int dtype, int64_t B, int64_t V, int64_t 
     // with many waves (C4) K1's rows already interleave and its 8 streaming
     // warps win (profiles/r2/k1p_ab.txt)
     const bool force = plan_host && (plan_host->flags & DP_PLAN_FORCE_PERSIST);
-    if (pg > 0 && ((B > pg && B <= 2 * (int64_t)pg) || force)) e = dp::launch_persist(a, dtype, pg, st);
+#ifdef DP_PERSIST_BALANCE   // A-B: every CTA takes the same number of rows (ceil(B / waves))
+    int pgrid = pg;
+    if (pg > 0) {
+      const int64_t waves = (B + pg - 1) / pg;
+      pgrid = (int)((B + waves - 1) / waves);
+    }
+#else
+    const int pgrid = pg;
+#endif
+    if (pg > 0 && ((B > pg && B <= 2 * (int64_t)pg) || force)) e = dp::launch_persist(a, dtype, pgrid, st);
     else e = dp::launch_topk(a, dtype, dp::kFull, (int)B, st);
     if (e != cudaSuccess) return cuda_status(e, "dp_sample_full/topk");
   }

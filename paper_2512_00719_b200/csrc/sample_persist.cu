@@ -28,7 +28,11 @@
 
 namespace dp {
 
-constexpr int kPNT = 256;            // threads per CTA
+#ifndef DP_PERSIST_NT
+#define DP_PERSIST_NT 256
+#define DP_PERSIST_MINB 4
+#endif
+constexpr int kPNT = DP_PERSIST_NT;  // threads per CTA
 #ifndef DP_PERSIST_SW
 #define DP_PERSIST_SW 5
 #endif
@@ -158,7 +162,7 @@ DP_DEV void all_hands(const SampleArgs& a, uint8_t* smem, const PersistLayout& L
 }
 
 template <typename T, int U>
-__global__ void __launch_bounds__(kPNT, 4) topk_persist_kernel(SampleArgs a) {
+__global__ void __launch_bounds__(kPNT, DP_PERSIST_MINB) topk_persist_kernel(SampleArgs a) {
   constexpr int EPV = Elem<T>::kPerVec;
   extern __shared__ __align__(16) uint8_t smem[];
   const PersistLayout L = persist_layout(a.wcap, a.kcap, a.lcap);
