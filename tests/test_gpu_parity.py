@@ -781,6 +781,54 @@ def test_c2_long_prompts_match_oracle(torch_cuda, variant):
     _big_batch_parity(torch_cuda, 152064, 1024, False, False, variant, 2048, 64, iters=2, prompt_len=2048)
 
 
+@pytest.mark.parametrize("variant", ["full", "shvs"])
+def test_long_prompts_nucleus_and_wide_rows_match_oracle(torch_cuda, variant):
+    """2,048-token prompts with rows that have no top-k (top-p only, min-p
+    only, neutral) and wide top-k (300): the penalty-excluding instantiation
+    with nucleus rows (256-list + fallback) and the radix-kept penalized
+    entries.  V = 32,000, 96 rows, every row checked over 3 iterations."""
+    torch = torch_cuda
+    from paper_2512_00719_b200 import DecisionPlane, HotVocab, SamplingParams
+    from paper_2512_00719_b200.synthetic import SyntheticSource
+
+    v, bsz = 32000, 96
+    kinds = [dict(temperature=0.9, top_p=0.8, rep_penalty=1.3, presence_penalty=0.4, frequency_penalty=0.2),
+             dict(temperature=0.7, min_p=0.02, rep_penalty=0.8, presence_penalty=-0.5),
+             dict(temperature=1.1, rep_penalty=1.2, frequency_penalty=0.3),
+             dict(temperature=0.8, top_k=300, top_p=0.95, rep_penalty=1.1, presence_penalty=1.5),
+             dict(temperature=0.8, top_k=50, rep_penalty=1.1, presence_penalty=0.5, frequency_penalty=0.1)]
+    params = [O.Params(**kinds[b % len(kinds)], seed=b) for b in range(bsz)]
+    prompts = [np.random.default_rng(b).integers(0, v, 2048) for b in range(bsz)]
+    src = SyntheticSource(v, device="cuda")
+    hot = HotVocab(v, src.hot_ordering()[:2048]) if variant == "shvs" else None
+    plane = DecisionPlane(v, [SamplingParams(**vars(p)) for p in params], prompts=prompts, hot=hot)
+    states = [O.State.new(prompts[b], v) for b in range(bsz)]
+    tail = O.tail_ids_of(hot.hot_ids, v) if hot is not None else None
+    perm = hot.device_maps(plane.device)[0] if hot is not None else None
+    exempt = []
+    for it in range(3):
+        x = src.generate(it, range(bsz), perm=perm)
+        if variant == "shvs":
+            d = plane.sample(x, it, variant="shvs")
+        else:
+            d = plane.sample(x, it)
+        tok, lp = d.token.cpu().numpy(), d.logprob.cpu().numpy()
+        xh = x.cpu().numpy()
+        if hot is not None:
+            xh = xh[:, hot.inv_perm]
+        dec = []
+        for b in range(bsz):
+            u = O.uniforms_per_row([params[b].seed], it, [b])[0]
+            if variant == "shvs":
+                dec.append(O.sample_shvs_row(xh[b], states[b], params[b], u, hot.hot_ids, tail))
+            else:
+                dec.append(O.sample_full_row(xh[b], states[b], params[b], u))
+        compare(f"longnuc/{variant}/it{it}", tok, lp, dec, exempt, lp_tol=1e-6)
+        for b in range(bsz):
+            states[b].update(int(tok[b]))
+    print("exemptions:", exempt)
+
+
 @pytest.mark.parametrize("raw", [False, True, "synth"])
 def test_c2_shvs_bench_config_matches_oracle(torch_cuda, raw):
     """The bench's SHVS line: C2 at full size, H=4,096 hot head; the summary
