@@ -86,7 +86,21 @@ DP_DEV void for_each_elem(const T* rowp, int64_t n, uint32_t tid, F fn) {
   for (int64_t i = tid; i < a0; i += kGenNT) fn(i, Elem<T>::get(rowp, i));
   const int64_t nvec = (n - a0) / EPV;
   const uint4* vp = reinterpret_cast<const uint4*>(rowp + a0);
-  for (int64_t v = tid; v < nvec; v += kGenNT) {
+  // kGenU independent 16-byte loads in flight per thread: one CTA walks a
+  // whole row per pass, so a single outstanding load per thread made every
+  // pass L2-latency-bound
+  constexpr int kGenU = 4;
+  int64_t v = tid;
+  for (; v + (kGenU - 1) * kGenNT < nvec; v += kGenU * kGenNT) {
+    uint4 q[kGenU];
+#pragma unroll
+    for (int u = 0; u < kGenU; ++u) q[u] = __ldg(vp + v + u * kGenNT);
+#pragma unroll
+    for (int u = 0; u < kGenU; ++u)
+#pragma unroll
+      for (int e = 0; e < EPV; ++e) fn(a0 + (v + u * kGenNT) * EPV + e, vec_elem<T>(q[u], e));
+  }
+  for (; v < nvec; v += kGenNT) {
     const uint4 q = __ldg(vp + v);
 #pragma unroll
     for (int e = 0; e < EPV; ++e) fn(a0 + v * EPV + e, vec_elem<T>(q, e));
