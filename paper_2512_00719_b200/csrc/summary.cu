@@ -182,7 +182,24 @@ __global__ void __launch_bounds__(NT) hot_mass_curve_kernel(const T* logits, int
   for (int32_t g = 0; g < n_grid; ++g) {
     const int64_t hi = grid[g];
     double s = 0.0;
-    for (int64_t pos = lo + threadIdx.x; pos < hi; pos += NT) {
+    // 4 independent loads in flight per thread (one at a time was L2/HBM
+    // latency-bound)
+    int64_t pos = lo + threadIdx.x;
+    for (; pos + 3 * NT < hi; pos += 4 * NT) {
+      float v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t q = pos + u * NT;
+        v[u] = Elem<T>::get(x, col_of_pos ? (int64_t)col_of_pos[q] : q);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t q = pos + u * NT;
+        if (plen > 0 && ((bitmap[q >> 5] >> (q & 31)) & 1u)) continue;
+        s += (double)expf(((v[u] - c_hi) - c_lo) * inv_tau);
+      }
+    }
+    for (; pos < hi; pos += NT) {
       if (plen > 0 && ((bitmap[pos >> 5] >> (pos & 31)) & 1u)) continue;
       const float v = Elem<T>::get(x, col_of_pos ? (int64_t)col_of_pos[pos] : pos);
       s += (double)expf(((v - c_hi) - c_lo) * inv_tau);
