@@ -53,7 +53,9 @@ struct PBuf {            // one candidate buffer's row description (streamers ->
   uint32_t overflow;
   uint32_t nscal;        // scalar head / tail keys in scal[]
   uint32_t n_valid;      // keys >= thr among the buffer's elements + scal
+  uint32_t dense;        // n_valid keys compacted at the buffer's unused slots (dense_of)
   uint64_t thr;          // admission threshold (composite key)
+  uint64_t kor, kand;    // OR / AND of the valid keys (constant-digit skipping)
   uint64_t scal[16];     // <= 2 * EPV - 2 = 14 keys (bf16)
   uint64_t tl0, tl1;     // DP_TIMELINE: row start / hand-over (globaltimer)
 };
@@ -68,6 +70,7 @@ struct PersistSmem {
   PBuf buf[2];
   float thr_warp[kPSW], est_warp[kPSW];
   uint32_t tmp;                 // streamers' count scratch
+  unsigned long long kor_s, kand_s;
   uint32_t bcast_s[4];          // streamers' select broadcast (overflow path)
   uint32_t bcast_f[4];          // finishers' select broadcast
   uint32_t nsel;
@@ -135,12 +138,24 @@ DP_DEV void all_hands(const SampleArgs& a, uint8_t* smem, const PersistLayout& L
   auto sync = [] { __syncthreads(); };
   uint32_t* hist = reinterpret_cast<uint32_t*>(smem + L.hist_f);
   uint64_t* sel = reinterpret_cast<uint64_t*>(smem + L.sel);
-  const uint64_t t = group_select_threshold<kPNT>(get_c, ns, pb.n_valid, kp, hist, ms.bcast_f, tid, sync);
+  const uint64_t* dense = reinterpret_cast<const uint64_t*>(cvec + min(pb.cnt, ccap));
+  auto get_d = [&](uint32_t i, uint64_t& key) -> bool { key = dense[i]; return true; };
+  const uint64_t kvar = pb.kor ^ pb.kand;
+  const uint64_t t = pb.dense
+                         ? group_select_threshold<kPNT>(get_d, pb.n_valid, pb.n_valid, kp, hist, ms.bcast_f, tid,
+                                                        sync, kvar, pb.kand)
+                         : group_select_threshold<kPNT>(get_c, ns, pb.n_valid, kp, hist, ms.bcast_f, tid, sync, kvar,
+                                                        pb.kand);
   if (tid == 0) ms.nsel = 0u;
   __syncthreads();
-  for (uint32_t i = tid; i < ns; i += kPNT) {
-    uint64_t kk;
-    if (get_c(i, kk) && kk >= t) sel[atomicAdd(&ms.nsel, 1u)] = kk;
+  if (pb.dense) {
+    for (uint32_t i = tid; i < pb.n_valid; i += kPNT)
+      if (dense[i] >= t) sel[atomicAdd(&ms.nsel, 1u)] = dense[i];
+  } else {
+    for (uint32_t i = tid; i < ns; i += kPNT) {
+      uint64_t kk;
+      if (get_c(i, kk) && kk >= t) sel[atomicAdd(&ms.nsel, 1u)] = kk;
+    }
   }
   __syncthreads();
 #ifdef DP_TIMELINE
@@ -236,6 +251,8 @@ __global__ void __launch_bounds__(kPNT, DP_PERSIST_MINB) topk_persist_kernel(Sam
         return key >= thr;
       };
       uint32_t n_valid = 0;
+      uint64_t kor = 0ull, kand = 0ull;
+      bool dense_ok = false;
       for (int pass_no = 0;; ++pass_no) {
         if (tid == 0) loaded += (uint64_t)nvec * 16u + (uint64_t)(a0 + (n - tail0)) * sizeof(T);
         int32_t base = (int32_t)warp * 32 * U;
@@ -356,25 +373,22 @@ __global__ void __launch_bounds__(kPNT, DP_PERSIST_MINB) topk_persist_kernel(Sam
         }
         sync_s();
         // keys >= thr in the buffer (+ scalars)
-        const uint32_t n_slots = min(pb.cnt, ccap) * EPV + pb.nscal;
-        if (tid == 0) ms.tmp = 0u;
-        sync_s();
-        uint32_t c = 0;
-        for (uint32_t i = tid; i < n_slots; i += kPSNT) {
-          uint64_t kk;
-          c += get_c(i, kk) ? 1u : 0u;
-        }
-        c = warp_sum(c);
-        if (lane == 0) atomicAdd(&ms.tmp, c);
-        sync_s();
-        n_valid = ms.tmp;
         const bool overflow = pb.overflow != 0u;
+        const uint32_t nc = min(pb.cnt, ccap);
+        const uint32_t dcap = overflow ? 0u : (ccap - nc) * 2u;
+        const DenseStats ds = group_compact_valid<kPSNT>(get_c, nc * EPV + pb.nscal,
+                                                         reinterpret_cast<uint64_t*>(cvec + nc), dcap, &ms.tmp,
+                                                         &ms.kor_s, &ms.kand_s, tid, sync_s);
+        n_valid = ds.n;
+        kor = ds.kor;
+        kand = ds.kand;
+        dense_ok = n_valid <= dcap;
         bool again = false;
         if (overflow) {
           // the buffer holds a subset of the admitted elements: its kp-th largest
           // key is a valid, strictly higher threshold
           const uint64_t t1 = group_select_threshold<kPSNT>(get_c, ccap * EPV + pb.nscal, n_valid, kp, hist_s,
-                                                            ms.bcast_s, tid, sync_s);
+                                                            ms.bcast_s, tid, sync_s, kor ^ kand, kand);
           if (t1 > thr) thr = t1;
           again = true;
         } else if (n_valid < kp && thr_f > t_lb) {
@@ -395,6 +409,9 @@ __global__ void __launch_bounds__(kPNT, DP_PERSIST_MINB) topk_persist_kernel(Sam
       if (tid == 0) {
         pb.thr = thr;
         pb.n_valid = n_valid;
+        pb.dense = dense_ok ? 1u : 0u;
+        pb.kor = kor;
+        pb.kand = kand;
         touch_bytes(a, row, loaded);
 #ifdef DP_TIMELINE
         pb.tl1 = gtimer();
@@ -450,13 +467,25 @@ __global__ void __launch_bounds__(kPNT, DP_PERSIST_MINB) topk_persist_kernel(Sam
         key = comp_key(x, (uint32_t)cidx[i / EPV] + i % EPV);
         return key >= thr;
       };
-      // exact top-kp of the row's candidates (unique composite keys)
-      const uint64_t t = group_select_threshold<kPFNT>(get_c, ns, pb.n_valid, kp, hist_f, ms.bcast_f, ft, sync_f);
+      // exact top-kp of the row's candidates (unique composite keys): from the
+      // streamers' dense copy of the valid keys when it fit
+      const uint64_t* dense = reinterpret_cast<const uint64_t*>(cvec + min(pb.cnt, ccap));
+      auto get_d = [&](uint32_t i, uint64_t& key) -> bool { key = dense[i]; return true; };
+      const uint64_t kvar = pb.kor ^ pb.kand;
+      const uint64_t t = pb.dense ? group_select_threshold<kPFNT>(get_d, pb.n_valid, pb.n_valid, kp, hist_f,
+                                                                  ms.bcast_f, ft, sync_f, kvar, pb.kand)
+                                  : group_select_threshold<kPFNT>(get_c, ns, pb.n_valid, kp, hist_f, ms.bcast_f, ft,
+                                                                  sync_f, kvar, pb.kand);
       if (ft == 0) ms.nsel = 0u;
       sync_f();
-      for (uint32_t i = ft; i < ns; i += kPFNT) {
-        uint64_t kk;
-        if (get_c(i, kk) && kk >= t) sel[atomicAdd(&ms.nsel, 1u)] = kk;
+      if (pb.dense) {
+        for (uint32_t i = ft; i < pb.n_valid; i += kPFNT)
+          if (dense[i] >= t) sel[atomicAdd(&ms.nsel, 1u)] = dense[i];
+      } else {
+        for (uint32_t i = ft; i < ns; i += kPFNT) {
+          uint64_t kk;
+          if (get_c(i, kk) && kk >= t) sel[atomicAdd(&ms.nsel, 1u)] = kk;
+        }
       }
       sync_f();
       const uint32_t nsel = ms.nsel;

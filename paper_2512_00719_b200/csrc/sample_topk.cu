@@ -54,6 +54,7 @@ struct TopkSmem {
   uint32_t nl;
   uint32_t nscal;
   uint32_t tmp;
+  unsigned long long kor, kand;   // OR / AND of the valid candidate keys (group_compact_valid)
   uint64_t scal[64];          // scalar head/tail candidates (CTA 0; every rank of a sharded row: <= 8 fp32 / 4 bf16 shards)
   FinishScratch fin;
 };
@@ -268,22 +269,6 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
       for (int i = 0; i < EPV; i += 2 * st) e[i] += e[i + st];
     sh += (double)e[0];
   };
-  // number of valid slots of an indexed candidate source (block-wide)
-  auto count_valid = [&](auto get, uint32_t n_slots) -> uint32_t {
-    if (tid == 0) ms.tmp = 0u;
-    __syncthreads();
-    uint32_t c = 0;
-    for (uint32_t i = tid; i < n_slots; i += NT) {
-      uint64_t kk;
-      c += get(i, kk) ? 1u : 0u;
-    }
-    c = warp_sum(c);
-    if (lane == 0) atomicAdd(&ms.tmp, c);
-    __syncthreads();
-    const uint32_t r = ms.tmp;
-    __syncthreads();
-    return r;
-  };
   // scalar head / tail elements (at most 2*EPV-2) belong to CTA 0 (warp 0)
   uint32_t nscal_acc = 0u;   // warp 0: scalar keys appended so far this pass
   auto head_tail = [&](bool first) {
@@ -327,6 +312,11 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
   // element >= threshold (one aggregated atomic per lane per batch).
   float t_lb = -INFINITY;
   uint32_t n_valid = 0;
+  // the valid keys, compacted into the candidate region's unused slots
+  // (select rounds then read n_valid keys, not every element slot)
+  uint64_t* dense = nullptr;
+  uint32_t dcap = 0u;
+  DenseStats ds{};
   uint64_t loaded = 0;   // tid 0: bytes this CTA streamed for the row (every pass)
   for (int pass_no = 0;; ++pass_no) {
   nscal_acc = 0u;
@@ -469,13 +459,20 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
   }   // shards of this CTA
     __syncthreads();
     const bool overflow = ms.overflow != 0u;
-    n_valid = count_valid(get_c, min(ms.cnt, ccap) * EPV + (own_scal ? ms.nscal : 0u));
+    {
+      const uint32_t nc = min(ms.cnt, ccap);
+      dense = reinterpret_cast<uint64_t*>(cvec + nc);
+      dcap = overflow ? 0u : (ccap - nc) * 2u;
+      ds = group_compact_valid<NT>(get_c, nc * EPV + (own_scal ? ms.nscal : 0u), dense, dcap, &ms.tmp, &ms.kor,
+                                   &ms.kand, tid, [] { __syncthreads(); });
+      n_valid = ds.n;
+    }
     bool again = false;
     if (overflow) {
       // the buffer holds a subset of the admitted elements: its kp-th largest
       // key is a valid, strictly higher threshold
       const uint64_t t1 = block_select_threshold<NT>(get_c, ccap * EPV + (own_scal ? ms.nscal : 0u), n_valid,
-                                                     kp, bhist, ms.bcast);
+                                                     kp, bhist, ms.bcast, ds.kor ^ ds.kand, ds.kand);
       if (t1 > thr) thr = t1;
       again = true;
     } else if (n_valid < kp && thr_f > t_lb) {
@@ -500,9 +497,17 @@ __global__ void __launch_bounds__(NT, MODE == kTail ? 2 : 1024 / NT) topk_sample
 #endif
   if (tid == 0) touch_bytes(a, row, loaded);
   // ---- CTA-level exact top-kp
-  {
+  if (n_valid <= dcap) {
+    auto get_d = [&](uint32_t i, uint64_t& key) -> bool { key = dense[i]; return true; };
+    const uint64_t t = block_select_threshold<NT>(get_d, n_valid, n_valid, kp, bhist, ms.bcast, ds.kor ^ ds.kand,
+                                                  ds.kand);
+    for (uint32_t i = tid; i < n_valid; i += NT) {
+      const uint64_t kk = dense[i];
+      if (kk >= t) sel[atomicAdd(&ms.nsel, 1u)] = kk;
+    }
+  } else {
     const uint32_t ns = min(ms.cnt, ccap) * EPV + (own_scal ? ms.nscal : 0u);
-    const uint64_t t = block_select_threshold<NT>(get_c, ns, n_valid, kp, bhist, ms.bcast);
+    const uint64_t t = block_select_threshold<NT>(get_c, ns, n_valid, kp, bhist, ms.bcast, ds.kor ^ ds.kand, ds.kand);
     for (uint32_t i = tid; i < ns; i += NT) {
       uint64_t kk;
       if (get_c(i, kk) && kk >= t) sel[atomicAdd(&ms.nsel, 1u)] = kk;

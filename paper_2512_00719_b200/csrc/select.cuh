@@ -123,12 +123,22 @@ DP_DEV uint32_t warp_compact(uint64_t* buf, uint32_t cnt, uint64_t t) {
 // empty slots, i in [0, n_slots).  NT cooperating threads (index t) with
 // barrier `sync`; hist: 256 u32 shared; bcast: 4 u32 shared.  Returns the
 // threshold to all.
+// kvar: the key bits that vary among the candidates (OR ^ AND over them, ~0
+// when unknown); a digit with no varying bit is the same for every key, so
+// its round is skipped (bf16 values: two of the four value digits are
+// constant, and positions < 2^24 leave the top position digit constant).
 template <int NT, typename Get, typename Sync>
 DP_DEV uint64_t group_select_threshold(Get get, uint32_t n_slots, uint32_t cnt, uint32_t need, uint32_t* hist,
-                                       uint32_t* bcast, uint32_t t, Sync sync) {
+                                       uint32_t* bcast, uint32_t t, Sync sync, uint64_t kvar = ~0ull,
+                                       uint64_t kconst = 0ull) {
   if (cnt <= need || need == 0) return need == 0 ? ~0ull : 0ull;
   uint64_t prefix = 0, mask = 0;
   for (int shift = 56; shift >= 0; shift -= 8) {
+    if (((kvar >> shift) & 255ull) == 0ull) {
+      prefix |= kconst & (255ull << shift);
+      mask |= 255ull << shift;
+      continue;
+    }
     for (uint32_t i = t; i < 256; i += NT) hist[i] = 0u;
     sync();
     for (uint32_t i = t; i < n_slots; i += NT) {
@@ -157,8 +167,64 @@ DP_DEV uint64_t group_select_threshold(Get get, uint32_t n_slots, uint32_t cnt, 
 
 template <int NT, typename Get>
 DP_DEV uint64_t block_select_threshold(Get get, uint32_t n_slots, uint32_t cnt, uint32_t need, uint32_t* hist,
-                                       uint32_t* bcast) {
-  return group_select_threshold<NT>(get, n_slots, cnt, need, hist, bcast, threadIdx.x, [] { __syncthreads(); });
+                                       uint32_t* bcast, uint64_t kvar = ~0ull, uint64_t kconst = 0ull) {
+  return group_select_threshold<NT>(get, n_slots, cnt, need, hist, bcast, threadIdx.x, [] { __syncthreads(); }, kvar,
+                                    kconst);
+}
+
+// The valid keys of an indexed candidate source, compacted (any order) into
+// dense[0, dcap) — the candidates' spare shared memory — with their count
+// and the OR / AND of the keys (constant-digit skipping above).  Every
+// later select round then reads n_valid dense keys instead of re-decoding
+// every element slot of the admitted vectors.  NT threads, index t; all of
+// them call it (warp ballots).  Returns the count; keys past dcap are not
+// stored (the caller then keeps the indexed source).
+struct DenseStats {
+  uint32_t n;
+  uint64_t kor, kand;
+};
+template <int NT, typename Get, typename Sync>
+DP_DEV DenseStats group_compact_valid(Get get, uint32_t n_slots, uint64_t* dense, uint32_t dcap, uint32_t* counter,
+                                      unsigned long long* kor_s, unsigned long long* kand_s, uint32_t t, Sync sync) {
+  const uint32_t lane = t & 31u;
+  if (t == 0) {
+    *counter = 0u;
+    *kor_s = 0ull;
+    *kand_s = ~0ull;
+  }
+  sync();
+  uint64_t o = 0ull, an = ~0ull;
+  for (uint32_t b0 = 0; b0 < n_slots; b0 += NT) {
+    const uint32_t i = b0 + t;
+    uint64_t kk = 0ull;
+    const bool v = i < n_slots && get(i, kk);
+    const uint32_t m = __ballot_sync(0xffffffffu, v);
+    uint32_t base = 0u;
+    if (lane == 0 && m) base = atomicAdd(counter, (uint32_t)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (v) {
+      const uint32_t s = base + (uint32_t)__popc(m & lanemask_lt());
+      if (s < dcap) dense[s] = kk;
+      o |= kk;
+      an &= kk;
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    o |= __shfl_xor_sync(0xffffffffu, o, off);
+    an &= __shfl_xor_sync(0xffffffffu, an, off);
+  }
+  if (lane == 0) {
+    atomicOr(kor_s, (unsigned long long)o);
+    atomicAnd(kand_s, (unsigned long long)an);
+  }
+  sync();
+  DenseStats r;
+  r.n = *counter;
+  r.kor = *kor_s;
+  r.kand = *kand_s;
+  sync();
+  return r;
 }
 
 }  // namespace dp
