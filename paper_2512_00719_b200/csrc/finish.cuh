@@ -378,10 +378,20 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
   // rank merge (O(nsel^2 / NT) compares per thread) for short candidate lists;
   // longer ones (long penalty lists: kp = k + |list|) take the radix cut +
   // register sort of one warp
+// Rank sort when nsel^2 / NT compares per thread stay small.  On an idle SM
+// (latency: the SHVS hot / tail passes) it beats the one-warp radix cut +
+// register sort up to ~240 compares per thread (tools/micro/finish_only.cu:
+// NT 96, nsel 80: 20.9k -> 9.8k cycles; NT 256, nsel 150: 20.9k -> 13.6k;
+// SHVS C2 71.3 -> 70.0 us).  With full rows streaming beside it (throughput:
+// K1 / K1p) its extra issue slots cost more than they save (C4 unchanged,
+// C2 +0.4 us at 240), so the full path keeps the tighter bound.
 #ifndef DP_RANK_MAX_ITERS
 #define DP_RANK_MAX_ITERS 48
 #endif
-  const bool fast = nsel * nsel <= (uint32_t)DP_RANK_MAX_ITERS * NT;
+#ifndef DP_RANK_MAX_ITERS_SHVS
+#define DP_RANK_MAX_ITERS_SHVS 240
+#endif
+  const bool fast = nsel * nsel <= (uint32_t)(MODE == kFull ? DP_RANK_MAX_ITERS : DP_RANK_MAX_ITERS_SHVS) * NT;
   // with the penalized ids outside the stream the fast path keeps them only
   // once the k-th unpenalized ready value rk is known: one pass, entries
   // >= rk (late_pen); the other paths pick the k best by a radix threshold

@@ -5,90 +5,36 @@
 #include <cstdlib>
 #include <vector>
 #include "../../paper_2512_00719_b200/csrc/finish.cuh"
+#ifndef FNT
+#define FNT 256
+#endif
 using namespace dp;
 
 template <int MB>
-__global__ void __launch_bounds__(256, MB) kern(SampleArgs a, const float* row, int n, int plen, int nsel_in,
+__global__ void __launch_bounds__(FNT, MB) kern(SampleArgs a, const float* row, int n, int plen, int nsel_in,
                                                 long long* cyc) {
   extern __shared__ __align__(16) uint8_t smem[];
   const FinLayout F = fin_layout(a.lcap);
   __shared__ uint64_t sel[1024];
   __shared__ FinishScratch fs;
   const uint32_t t = threadIdx.x;
-  // candidate keys: the nsel largest of the row (by value)
-  for (int i = t; i < nsel_in; i += 256) sel[i] = comp_key(row[i], (uint32_t)i);
+  for (int i = t; i < nsel_in; i += FNT) sel[i] = comp_key(row[i], (uint32_t)i);
   const dp_params_t p = a.params[0];
   __syncthreads();
-  {   // the draw with a COLD instruction cache: first code this kernel runs after setup
-    const double* frc = reinterpret_cast<const double*>(smem + F.r);
-    for (int i = t; i < 64; i += 256) reinterpret_cast<double*>(smem + F.r)[i] = -0.05 * i;
-    __syncthreads();
-    if (t < 32) {
-      long long c0 = clock64();
-      DrawResult d = warp_filter_draw(frc, 50, knobs_of(p), 0.37, reinterpret_cast<double*>(smem + F.w),
-                                      reinterpret_cast<double*>(smem + F.cum), nullptr);
-      long long c1 = clock64();
-      if (t == 0) { cyc[6] = c1 - c0; if (d.index == -3) cyc[7] = 2; }
-    }
-    __syncthreads();
-  }
-#ifdef DP_DRAW_PROBE
-  if (t == 0) g_probe_base = 0;
-#endif
-  __syncthreads();
   long long t0 = clock64();
-  long long inter = 0;
-  for (int it = 0; it < 4; ++it) {
-    finish_row<float, kFull, 256, false, false>(a, 0, p, plen, row, 0, n, sel, nsel_in, 0.0, 0.0, smem, F, fs, t,
+  for (int it = 0; it < 16; ++it) {
+    finish_row<float, kFull, FNT, false, false>(a, 0, p, plen, row, 0, n, sel, nsel_in, 0.0, 0.0, smem, F, fs, t,
                                   [] { __syncthreads(); });
-    __syncthreads();
-    // the same draw right after finish_row, interleaved (i-cache probe)
-    if (t < 32) {
-      const double* fr0 = reinterpret_cast<const double*>(smem + F.r);
-#ifdef DP_DRAW_PROBE
-      if (t == 0) g_probe_base = 8;  // standalone copy
-#endif
-      __syncwarp();
-      long long q0 = clock64();
-      if (t == 0) atomicAdd((unsigned long long*)&a.dbg.stats[20], 1ull);   // like lap(14) right before the draw
-      DrawResult d = warp_filter_draw(fr0, p.top_k, knobs_of(p), 0.41, reinterpret_cast<double*>(smem + F.w),
-                                      reinterpret_cast<double*>(smem + F.cum), nullptr);
-      long long q1 = clock64();
-      inter += q1 - q0;
-      if (d.index == -5) cyc[7] = 1;
-#ifdef DP_DRAW_PROBE
-      if (t == 0) g_probe_base = 0;
-#endif
-      __syncwarp();
-    }
     __syncthreads();
   }
   long long t1 = clock64();
-  if (t == 0) { cyc[0] = (t1 - t0) / 4; cyc[5] = inter / 4; }
-  // the draw alone, on the final list finish_row left in shared memory
-  double* fr = reinterpret_cast<double*>(smem + F.r);
-  double* fw = reinterpret_cast<double*>(smem + F.w);
-  double* fc = reinterpret_cast<double*>(smem + F.cum);
-  __syncthreads();
-  if (t < 32) {
-    double acc = 0;
-    long long d0 = clock64();
-    for (int it = 0; it < 10; ++it) {
-      DrawResult d = warp_filter_draw(fr, p.top_k, knobs_of(p), 0.3 + 1e-3 * it, fw, fc, a.dbg.stats);
-      acc += d.logprob;
-    }
-    long long d1 = clock64();
-    if (t == 0) { cyc[1] = (d1 - d0) / 10; cyc[3] = (long long)acc; }
-    d0 = clock64();
-    DrawResult d = warp_filter_draw(fr, p.top_k, knobs_of(p), 0.77, fw, fc, a.dbg.stats);
-    d1 = clock64();
-    if (t == 0) { cyc[2] = d1 - d0; cyc[4] = d.index; }
-  }
+  if (t == 0) { cyc[0] = (t1 - t0) / 16; cyc[1] = cyc[2] = cyc[5] = cyc[6] = 0; }
 }
 
 int main(int argc, char** argv) {
   const int nblk = argc > 1 ? atoi(argv[1]) : 1;
-  const int n = 8192, plen = 100, cap = 256, nsel = 150;
+  const int n = 8192, cap = 256;
+  const int nsel = argc > 2 ? atoi(argv[2]) : 150, plen = argc > 3 ? atoi(argv[3]) : 100;
   std::vector<float> h(n);
   for (int i = 0; i < n; ++i) h[i] = (i < 1000) ? 5.0f - 0.004f * i : -3.0f - 1e-4f * i;
   float* row; cudaMalloc(&row, n * 4); cudaMemcpy(row, h.data(), n * 4, cudaMemcpyHostToDevice);
@@ -110,20 +56,20 @@ int main(int argc, char** argv) {
   a.logits = row; a.ld = n; a.V = n; a.H = 0; a.params = d_p;
   a.pen.ids = d_ids; a.pen.out_count = d_cnt; a.pen.len = d_len; a.pen.prompt_len = d_plen; a.pen.cap = cap;
   a.pen.vocab_size = n; a.uniforms = d_u; a.n_rows = 1; a.token = tok; a.logprob = lp; a.flags = fl;
-  a.dbg.stats = (int64_t*)st;
+  a.dbg.stats = getenv("LAPS") ? (int64_t*)st : nullptr;
   a.kcap = 256; a.lcap = 512; a.wcap = 1024; a.split = 1; a.nt = 256;
   const FinLayout F = fin_layout(a.lcap);
   for (int mb : {1, 2, 4}) {
     for (int rep = 0; rep < 2; ++rep) {
-      if (mb == 1) { cudaFuncSetAttribute(kern<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, F.bytes); kern<1><<<nblk, 256, F.bytes>>>(a, row, n, plen, nsel, cyc); }
-      if (mb == 2) { cudaFuncSetAttribute(kern<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, F.bytes); kern<2><<<nblk, 256, F.bytes>>>(a, row, n, plen, nsel, cyc); }
-      if (mb == 4) { cudaFuncSetAttribute(kern<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, F.bytes); kern<4><<<nblk, 256, F.bytes>>>(a, row, n, plen, nsel, cyc); }
+      if (mb == 1) { cudaFuncSetAttribute(kern<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, F.bytes); kern<1><<<nblk, FNT, F.bytes>>>(a, row, n, plen, nsel, cyc); }
+      if (mb == 2) { cudaFuncSetAttribute(kern<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, F.bytes); kern<2><<<nblk, FNT, F.bytes>>>(a, row, n, plen, nsel, cyc); }
+      if (mb == 4) { cudaFuncSetAttribute(kern<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, F.bytes); kern<4><<<nblk, FNT, F.bytes>>>(a, row, n, plen, nsel, cyc); }
       cudaError_t e = cudaDeviceSynchronize();
       if (e != cudaSuccess) { printf("err %s\n", cudaGetErrorString(e)); return 1; }
     }
     int tk; cudaMemcpy(&tk, tok, 4, cudaMemcpyDeviceToHost);
     printf("  laps/row:");
-    for (int sl : {8, 12, 9, 10, 11, 13, 14, 16, 15}) printf(" %d:%lld", sl, st[sl] / (8 * nblk));
+    for (int sl : {8, 12, 9, 10, 11, 13, 14, 16, 15}) printf(" %d:%lld", sl, st[sl] / (32 * nblk));
     printf("\n");
     for (int i = 0; i < 24; ++i) st[i] = 0;
     printf("[%d CTAs] finish_row minBlocks=%d: %lld cycles (token %d); draw in loop %lld, draw once %lld, draw interleaved with finish_row %lld, draw COLD %lld\n", nblk, mb, cyc[0], tk, cyc[1], cyc[2], cyc[5], cyc[6]);
