@@ -6,8 +6,12 @@ rep, binary, kname = sys.argv[1:4]
 n = int(sys.argv[4]) if len(sys.argv) > 4 else 40
 d = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(binary)], cwd=d, capture_output=True)
-cub = [f for f in os.listdir(d) if f.endswith(".cubin")][0]
-sass = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(d, cub)], capture_output=True, text=True).stdout
+sass = ""
+for cub in sorted(f for f in os.listdir(d) if f.endswith(".cubin")):
+    names = subprocess.run(["cuobjdump", "-symbols", os.path.join(d, cub)], capture_output=True, text=True).stdout
+    if kname in names:
+        sass = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(d, cub)], capture_output=True, text=True).stdout
+        break
 cur, a2l, inside = None, {}, False
 for ln in sass.splitlines():
     if ln.startswith(".text.") or ln.startswith("//---------------------"):
