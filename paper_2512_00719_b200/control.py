@@ -135,15 +135,20 @@ class HotSizeController:
         return self.cost
 
     def curve(self, logits, summary=None) -> sizing.HitRatioCurve:
-        """Mean hot mass along the master ordering at the grid sizes (K6 on
-        the current rows through the position map), plus alpha(V) = 1."""
+        """Mean hot mass along the master ordering at the grid sizes plus
+        H = 1 (K6 on the current rows through the position map), and
+        alpha(V) = 1: the curve spans [1, V] like fit-sizing's
+        `sorted(set(grid + [1, V]))` (cli.py:88).  Without the H = 1 point
+        np.interp holds alpha flat below the first grid size, Eq. 10 then
+        prices H = 1 at alpha(grid[0]), and the argmin lands on H = 1 whenever
+        c0 dominates (C1: V = 32k, 64 rows)."""
         plane = self.plane
         hot = plane.hot if plane.hot is not None else self.master
         if plane.hot is None:
             plane.set_hot(hot)
-        rows = plane.hot_mass_curve(logits, self.grid, summary=summary, order=self.master)
+        grid = sorted(set(self.grid) | {1})
+        rows = plane.hot_mass_curve(logits, grid, summary=summary, order=self.master)
         abar = rows.mean(dim=0).cpu().numpy()
-        grid = list(self.grid)
         v = plane.vocab_size
         if grid[-1] < v:
             grid.append(v)

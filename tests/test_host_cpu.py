@@ -225,3 +225,46 @@ def test_hot_size_controller_boundary_logic_on_cpu():
     assert abs(ctl.acceptance_rate() - 5 / 8) < 1e-12
     with pytest.raises(ValueError):
         ctl.refit(None)                 # no cost model yet
+
+
+def test_hot_size_controller_curve_spans_one_to_v():
+    """The controller's hit-ratio curve carries H = 1 and H = V like
+    fit-sizing's `sorted(set(grid + [1, V]))` (cli.py:88).  Without the H = 1
+    point np.interp holds alpha flat below the first grid size, and with a
+    dominant fixed cost c0 (C1 on a B200) Eq. 10's argmin lands on H = 1.  A
+    stand-in plane returns a known per-row curve (no kernels)."""
+    import torch
+
+    from paper_2512_00719_b200 import sizing
+    from paper_2512_00719_b200.control import HotSizeController
+    from paper_2512_00719_b200.shvs import HotVocab
+
+    v, bsz = 32000, 4
+
+    def alpha(h):   # hot mass of the first h ids: 0.30 at h = 1, 0.95 at 256, 1 at V
+        return min(1.0, 0.30 + 0.65 * np.log(h) / np.log(256)) if h < v else 1.0
+
+    class Plane:
+        vocab_size, batch = v, bsz
+
+        def __init__(self):
+            self.hot = None
+            self.asked = None
+
+        def set_hot(self, hot):
+            self.hot = hot
+
+        def hot_mass_curve(self, logits, grid, summary=None, order=None):
+            self.asked = list(grid)
+            return torch.tensor([[alpha(h) for h in grid]] * bsz, dtype=torch.float64)
+
+    plane = Plane()
+    master = HotVocab(v, np.arange(v))
+    # C1's fitted constants (bench_c1.jsonl): c0 = 5.7e-7 s per row, c = 5.0e-12 s per row-token
+    ctl = HotSizeController(plane, master, grid=(256, 512, 1024, 2048, 4096, 8192, 16384), cost=(5.7e-7, 5.0e-12))
+    h = ctl.refit(None)
+    assert plane.asked[0] == 1 and 256 in plane.asked
+    assert list(ctl.model.curve.grid[[0, -1]]) == [1.0, float(v)]
+    assert abs(ctl.model.curve.value(1.0) - alpha(1)) < 1e-12
+    assert h > 1
+    assert h == sizing.optimal_hot_size(ctl.model)
