@@ -696,6 +696,8 @@ def test_heavy_penalties_300_iterations_match_reference_run(torch_cuda, raw, for
 def _bench_params(cfg_mix, b):
     C2 = dict(temperature=0.8, top_k=50, top_p=0.9, min_p=0.05, rep_penalty=1.1, presence_penalty=0.5,
               frequency_penalty=0.1)
+    if cfg_mix == "c1":   # BASELINE configs[0]: top-k 50, top-p 0.9, repetition 1.1
+        return O.Params(temperature=0.8, top_k=50, top_p=0.9, rep_penalty=1.1, seed=0)
     if not cfg_mix:
         return O.Params(**C2, seed=0)
     mix = [dict(temperature=0.8, top_k=1), dict(temperature=0.8, top_k=50), dict(temperature=0.8, top_p=0.9),
@@ -835,6 +837,14 @@ def test_c2_shvs_bench_config_matches_oracle(torch_cuda, raw):
     exact and penalized (False), the producer's raw one from a separate pass
     (True), or emitted by the producer while writing the logits ("synth")."""
     _big_batch_parity(torch_cuda, 152064, 1024, False, False, "shvs", 4096, 8, raw=raw)
+
+
+@pytest.mark.parametrize("raw", [False, True, "synth"])
+def test_c1_shvs_at_model_hot_size_matches_oracle(torch_cuda, raw):
+    """C1 (V=32,000, B=64) through SHVS at the sizing model's H* = 512 (the
+    bench's C1 SHVS line since the curve spans [1, V]): every row, 4
+    iterations, 4-CTA tail clusters (V - H >= 16,384)."""
+    _big_batch_parity(torch_cuda, 32000, 64, False, "c1", "shvs", 512, 1, iters=4, raw=raw)
 
 
 def test_c5_mix_shvs_with_producer_fused_summary(torch_cuda):
