@@ -270,6 +270,15 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
   const uint32_t hmask = hcap - 1u;
   double u[3];
   get_uniforms(a, row, p, u);
+#ifdef DP_TIMELINE   // A-B build: globaltimer marks of the final stage's phases -> dbg.topk_ready[row * stride + 5..7]
+  uint64_t tm[4] = {0, 0, 0, 0};
+  auto tmark = [&](int i) {
+    if (t == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm[i]));
+  };
+#else
+  auto tmark = [](int) {};
+#endif
+  tmark(0);
   const bool prof = a.dbg.stats != nullptr && t == 0;
   long long pc = prof ? clock64() : 0;
   auto lap = [&](int slot) {
@@ -475,6 +484,7 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
     for (int w = 0; w < NT / 32; ++w) s_dom += fs.corr[w] - fs.sh_pen[w];   // fixed order
   }
   lap(12);
+  tmark(1);
   auto penalized = [&](uint32_t pos) -> bool {
     if (excl || plen == 0) return false;
     uint32_t h = (pos * 2654435761u) & hmask;
@@ -672,6 +682,7 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
   }
 
   lap(14);
+  tmark(2);
   if (warp == 0) {
     const double ud = u[MODE == kTail ? 2 : 0];
     // no usable mass: every candidate is -inf (DegenerateRowError, core.py:19-20)
@@ -689,6 +700,7 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
       d = warp_filter_draw(fr, (int32_t)min((uint32_t)k, nl), knobs_of(p), ud, fw, fcum, a.dbg.stats);
     }
     lap(16);
+    tmark(3);
 
     if (degen) {
       if (lane == 0) {
@@ -724,6 +736,14 @@ DP_DEV bool finish_row(const SampleArgs& a, int row, const dp_params_t& p, int32
   }
   sync();
   lap(15);
+#ifdef DP_TIMELINE   // (after the top-k debug values, which share the row's slots)
+  if (t == 0 && a.dbg.topk_ready && a.dbg.topk_stride >= 8) {
+    double* tl = a.dbg.topk_ready + (int64_t)row * a.dbg.topk_stride;
+    tl[5] = (double)(tm[1] - tm[0]);
+    tl[6] = (double)(tm[2] - tm[1]);
+    tl[7] = (double)(tm[3] - tm[2]);
+  }
+#endif
   return true;
 }
 
