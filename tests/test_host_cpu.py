@@ -268,3 +268,18 @@ def test_hot_size_controller_curve_spans_one_to_v():
     assert abs(ctl.model.curve.value(1.0) - alpha(1)) < 1e-12
     assert h > 1
     assert h == sizing.optimal_hot_size(ctl.model)
+
+
+def test_product_fails_loudly_without_library_or_device(tmp_path):
+    """No CPU fallback: a missing library raises NativeUnavailable at load,
+    and a DecisionPlane without a CUDA sm_100 device raises it at
+    construction (this container has no GPU)."""
+    import torch
+
+    from paper_2512_00719_b200 import DecisionPlane, SamplingParams, _native
+
+    with pytest.raises(_native.NativeUnavailable):
+        _native.load(str(tmp_path / "missing.so"))
+    if not torch.cuda.is_available():
+        with pytest.raises(_native.NativeUnavailable):
+            DecisionPlane(64, [SamplingParams(top_k=4, seed=0)], device="cuda:0")
