@@ -270,7 +270,7 @@ def test_hot_size_controller_curve_spans_one_to_v():
     assert h == sizing.optimal_hot_size(ctl.model)
 
 
-def test_product_fails_loudly_without_library_or_device(tmp_path):
+def test_product_fails_loudly_without_library_or_device(tmp_path, monkeypatch):
     """No CPU fallback: a missing library raises NativeUnavailable at load,
     and a DecisionPlane without a CUDA sm_100 device raises it at
     construction (this container has no GPU)."""
@@ -278,8 +278,10 @@ def test_product_fails_loudly_without_library_or_device(tmp_path):
 
     from paper_2512_00719_b200 import DecisionPlane, SamplingParams, _native
 
+    monkeypatch.setattr(_native, "_lib", None)   # as in a fresh process (another test may have loaded it)
     with pytest.raises(_native.NativeUnavailable):
         _native.load(str(tmp_path / "missing.so"))
+    monkeypatch.undo()
     if not torch.cuda.is_available():
         with pytest.raises(_native.NativeUnavailable):
             DecisionPlane(64, [SamplingParams(top_k=4, seed=0)], device="cuda:0")
